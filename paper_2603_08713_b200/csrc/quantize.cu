@@ -1,0 +1,562 @@
+// quantize.cu -- sm_100a quantizer kernels (K1-K4) and the dequantiser (K5).
+//
+// K1 quantize_pow2   OCP32 / MX16 / MX16_OAS   src/quantize.py:586-609
+// K2 quantize_mbs_s  MBS-Static                src/quantize.py:612-659, :383-406
+// K3 quantize_mbs_d  MBS-Dynamic (exact)       src/quantize.py:426-461
+// K4 quantize_nvfp4  two passes (amax, encode) src/quantize.py:662-706
+// K5 dequantize                                src/quantize.py:728-746
+//
+// All quantizers are HBM-bound streaming kernels except MBS-D (17 candidate
+// trials per macro, compute-bound).  One thread owns one 16-element block
+// (32 for OCP32): 128-bit loads of bf16/f32, warp-shuffle macro maxima, the
+// integer E8M0 closed form, hardware E2M1 pair conversion, one 8/16-byte code
+// store.  Scales are written row-major (the reference layout) and/or in the
+// tcgen05 SF-atom layout the GEMM's TMA reads directly.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "mxq_arith.cuh"
+#include "mxq_internal.h"
+
+namespace mxq {
+
+// ---------------------------------------------------------------------------
+// Loading one block of `N` elements as f32 (bf16 widened exactly).
+// ---------------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void load_block(const void* __restrict__ x, int dtype, int64_t off, float (&v)[N]) {
+  if (dtype == DT_BF16) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(x) + off);
+#pragma unroll
+    for (int q = 0; q < N / 8; ++q) {
+      uint4 w = __ldcs(p + q);
+      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[q * 8 + 2 * j] = __uint_as_float(ws[j] << 16);
+        v[q * 8 + 2 * j + 1] = __uint_as_float(ws[j] & 0xffff0000u);
+      }
+    }
+  } else {
+    const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x) + off);
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q) {
+      float4 w = __ldcs(p + q);
+      v[q * 4 + 0] = w.x; v[q * 4 + 1] = w.y; v[q * 4 + 2] = w.z; v[q * 4 + 3] = w.w;
+    }
+  }
+}
+
+template <int N>
+__device__ __forceinline__ float block_absmax(const float (&v)[N], bool& finite) {
+  float a = 0.0f;
+  uint32_t bad = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    uint32_t u = __float_as_uint(v[i]) & 0x7fffffffu;
+    bad |= (u >= 0x7f800000u);
+    a = fmaxf(a, __uint_as_float(u));
+  }
+  finite = !bad;
+  return a;
+}
+
+// Codes for N scaled values: scaled = v * sf (exact power-of-two f32 scaling;
+// a result that would be f32-subnormal is < 2^-126 and encodes to 0 either
+// way), packed two per byte, even element in the low nibble.
+template <int N>
+__device__ __forceinline__ void encode_block(const float (&v)[N], float sf, uint32_t (&packed)[N / 8]) {
+#pragma unroll
+  for (int w = 0; w < N / 8; ++w) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float lo = __fmul_rn(v[w * 8 + 2 * j], sf);
+      float hi = __fmul_rn(v[w * 8 + 2 * j + 1], sf);
+      word |= e2m1x2(lo, hi) << (8 * j);
+    }
+    packed[w] = word;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ void store_codes(uint8_t* __restrict__ dst, const uint32_t (&packed)[N / 8]) {
+  if constexpr (N == 16) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(packed[0], packed[1]);
+  } else {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  }
+}
+
+__device__ __forceinline__ void store_scale(const QDesc& q, int64_t r, int64_t kb, uint8_t s) {
+  if (q.scales) q.scales[r * q.scales_ld + kb] = s;
+  if (q.scales_mma) q.scales_mma[sf_mma_offset(r, kb, q.sf_kpad)] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K1: power-of-two variants.  Grid-stride over blocks; thread == block.
+// ---------------------------------------------------------------------------
+template <int BS, bool OCP, bool OAS>
+__global__ void __launch_bounds__(256) k_quantize_pow2(const void* __restrict__ x, int dtype, int64_t x_ld,
+                                                       QDesc q, uint32_t* __restrict__ status) {
+  const int64_t nbr = q.cols / BS;
+  const int64_t nb = q.rows * nbr;
+  uint32_t bad = 0;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = b / nbr, kb = b - r * nbr;
+    float v[BS];
+    load_block<BS>(x, dtype, r * x_ld + kb * BS, v);
+    bool fin;
+    float alpha = block_absmax<BS>(v, fin);
+    bad |= !fin;
+    uint8_t biased = OCP ? e8m0_biased_ocp(alpha) : e8m0_biased_16(alpha, OAS);
+    float sf = exp2i_f32(127 - (int)biased);
+    uint32_t packed[BS / 8];
+    encode_block<BS>(v, sf, packed);
+    store_codes<BS>(q.codes + r * q.codes_ld + kb * (BS / 2), packed);
+    store_scale(q, r, kb, biased);
+  }
+  if (bad) atomicOr(status, ST_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------
+// Macro-group geometry for MBS: G lanes (a power of two <= 32) own one macro
+// of up to 32 blocks (macro_size <= 512); a trailing partial macro simply has
+// fewer active lanes.  `gid` enumerates (row, macro) pairs.
+// ---------------------------------------------------------------------------
+struct MacroGeom {
+  int G;          // lanes per macro group
+  int64_t nmac;   // macros per row
+  int macro;      // macro width (elements)
+};
+
+__device__ __forceinline__ float group_max(float v, int G) {
+  for (int o = G / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ void store_mbs_outputs(const QDesc& q, int64_t r, int64_t mac, int64_t kb,
+                                                  const uint32_t (&packed)[2], uint8_t biased) {
+  store_codes<16>(q.codes + r * q.codes_ld + kb * 8, packed);
+  store_scale(q, r, kb, biased);
+}
+
+__device__ __forceinline__ void store_m8(const QDesc& q, int64_t r, int64_t mac, uint8_t m8) {
+  if (q.mant) q.mant[r * q.mant_ld + mac] = m8;
+  if (q.mant_t) q.mant_t[mac * q.mant_t_ld + r] = m8;
+}
+
+// Quantise one block (v, scaled by the f32 factor f) with OAS: the shared
+// second half of MBS-S and MBS-D (src/quantize.py:392-406).
+__device__ __forceinline__ uint8_t mbs_block(const float (&v)[16], float f, uint32_t (&packed)[2], bool& ovf) {
+  float y[16];
+  float a = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    y[i] = __fmul_rn(v[i], f);
+    a = fmaxf(a, fabsf(y[i]));
+  }
+  ovf = !(a <= 3.402823466e38f);
+  uint8_t biased = e8m0_biased_16(a, true);
+  encode_block<16>(y, exp2i_f32(127 - (int)biased), packed);
+  return biased;
+}
+
+// K2: MBS-Static.  The CTA-uniform `base` loop keeps every warp converged
+// for the group shuffles.
+__global__ void __launch_bounds__(256) k_quantize_mbs_s(const void* __restrict__ x, int dtype, int64_t x_ld,
+                                                        QDesc q, MacroGeom g, uint32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (g.G - 1);
+  const int64_t ngroups = q.rows * g.nmac;
+  const int64_t gpb = (int64_t)blockDim.x / g.G;  // groups per CTA pass
+  uint32_t bad = 0;
+  for (int64_t base = (int64_t)blockIdx.x * gpb; base < ngroups; base += (int64_t)gridDim.x * gpb) {
+    const int64_t gi = base + threadIdx.x / g.G;
+    const bool live_group = gi < ngroups;
+    const int64_t r = live_group ? gi / g.nmac : 0;
+    const int64_t mac = live_group ? gi - r * g.nmac : 0;
+    const int64_t c0 = mac * g.macro + (int64_t)sub * 16;
+    const int64_t width = live_group ? min((int64_t)g.macro, q.cols - mac * g.macro) : 0;
+    const bool active = live_group && sub * 16 < width;
+    float v[16];
+    if (active) load_block<16>(x, dtype, r * x_ld + c0, v);
+    else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    }
+    bool fin;
+    float a16 = block_absmax<16>(v, fin);
+    bad |= !fin;
+    const float amac = group_max(a16, g.G);
+    const uint8_t m8 = static_m8(amac);
+    uint32_t packed[2];
+    bool ovf;
+    const uint8_t biased = mbs_block(v, mbs_factor(m8), packed, ovf);
+    if (active) {
+      bad |= ovf ? 2u : 0u;
+      store_mbs_outputs(q, r, mac, c0 / 16, packed, biased);
+      if (sub == 0) store_m8(q, r, mac, m8);
+    }
+  }
+  if (bad & 1u) atomicOr(status, ST_NONFINITE);
+  if (bad & 2u) atomicOr(status, ST_OVERFLOW);
+}
+
+// ---------------------------------------------------------------------------
+// K3: MBS-Dynamic, exact mode.  For every candidate m8 (plus the static one
+// when augmenting) the macro is quantised and dequantised exactly as the
+// reference does, the f64 squared errors are staged in shared memory and one
+// lane per group reduces them in numpy's pairwise order, so the argmin (ties
+// to the smaller byte) is bit-identical to src/quantize.py:438-461.
+// ---------------------------------------------------------------------------
+constexpr int MBSD_THREADS = 128;
+constexpr int MBSD_STRIDE = 17;  // doubles per lane slot (16 + 1 pad)
+
+__device__ double pw_sum_smem(const double* lane_base, int64_t start, int64_t n);
+
+// Element p of a macro lives in lane p/16, slot p%16.
+__device__ __forceinline__ double sq_at(const double* base, int64_t p) {
+  return base[(p >> 4) * MBSD_STRIDE + (p & 15)];
+}
+
+__device__ double pw_leaf_smem(const double* base, int64_t s, int64_t n) {
+  if (n < 8) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, sq_at(base, s + i));
+    return acc;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = sq_at(base, s + j);
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq_at(base, s + i + j));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, sq_at(base, s + i));
+  return res;
+}
+
+__device__ double pw_sum_smem(const double* base, int64_t s, int64_t n) {
+  if (n <= 128) return pw_leaf_smem(base, s, n);
+  int64_t n2 = pw_split(n);
+  return __dadd_rn(pw_sum_smem(base, s, n2), pw_sum_smem(base, s + n2, n - n2));
+}
+
+__constant__ uint8_t c_cands[256];
+// LUT mode table (src/quantize.py:482-504): [regime][candidate][bin] fp16
+// values widened to f32 (exact).
+__constant__ float c_lut[2][16][64];
+
+// LUT=false: exact SSE search (src/quantize.py:438-461).
+// LUT=true : table-estimated cost sum(x^2 * T[v]) (src/quantize.py:507-542),
+//            v = |x| * SF(OAS scale of the candidate-scaled block).
+template <bool LUT>
+__global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __restrict__ x, int dtype, int64_t x_ld,
+                                                                 QDesc q, MacroGeom g, int n_cand, int augment,
+                                                                 uint32_t* __restrict__ status) {
+  __shared__ double s_sq[MBSD_THREADS * MBSD_STRIDE];
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (g.G - 1);
+  double* gbase = s_sq + (threadIdx.x - sub) * MBSD_STRIDE;  // this group's slots
+  double* mine = s_sq + threadIdx.x * MBSD_STRIDE;
+  const int64_t ngroups = q.rows * g.nmac;
+  const int64_t gpb = MBSD_THREADS / g.G;
+  uint32_t bad = 0;
+  for (int64_t base = (int64_t)blockIdx.x * gpb; base < ngroups; base += (int64_t)gridDim.x * gpb) {
+    const int64_t gi = base + threadIdx.x / g.G;
+    const bool live_group = gi < ngroups;
+    const int64_t r = live_group ? gi / g.nmac : 0;
+    const int64_t mac = live_group ? gi - r * g.nmac : 0;
+    const int64_t c0 = mac * g.macro + (int64_t)sub * 16;
+    const int64_t width = live_group ? min((int64_t)g.macro, q.cols - mac * g.macro) : 0;
+    const bool active = live_group && sub * 16 < width;
+    float v[16];
+    if (active) load_block<16>(x, dtype, r * x_ld + c0, v);
+    else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
+    }
+    bool fin;
+    float a16 = block_absmax<16>(v, fin);
+    bad |= !fin;
+    const float amac = group_max(a16, g.G);
+    const uint32_t m8_static = static_m8(amac);
+    const int n_trials = n_cand + (augment ? 1 : 0);
+    double best_sse = 0.0;
+    uint32_t best_m8 = 0;
+    for (int t = 0; t < n_trials; ++t) {
+      const uint32_t m8 = t < n_cand ? (uint32_t)c_cands[t] : m8_static;
+      const float f = mbs_factor(m8);
+      // quantise: y = x*f, OAS scale, codes
+      float y[16];
+      float a = 0.0f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        y[i] = __fmul_rn(v[i], f);
+        a = fmaxf(a, fabsf(y[i]));
+      }
+      const uint32_t biased = e8m0_biased_16(a, true);
+      const float sf = exp2i_f32(127 - (int)biased);
+      if constexpr (LUT) {
+        const double sf64 = ldexp(1.0, 127 - (int)biased);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const double x64 = (double)v[i];
+          const double vv = __dmul_rn(fabs(x64), sf64);
+          double tv;
+          if (vv < 1.0) {
+            long long b = (long long)__dmul_rn(vv, 64.0);
+            b = b < 0 ? 0 : (b > 63 ? 63 : b);
+            tv = (double)c_lut[0][t][b];
+          } else {
+            long long b = (long long)__ddiv_rn(__dmul_rn(__dsub_rn(vv, 1.0), 64.0), 7.0);
+            b = b < 0 ? 0 : (b > 63 ? 63 : b);
+            tv = (double)c_lut[1][t][b];
+          }
+          mine[i] = active ? __dmul_rn(__dmul_rn(x64, x64), tv) : 0.0;
+        }
+      } else {
+        const bool fast = biased >= 4 && biased <= 250;
+        float tq[8];
+        if (fast) {
+          const float d = exp2i_f32((int)biased - 127);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) tq[k] = __fmul_rn(__fdiv_rn(e2m1_grid(k), f), d);
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t c = (c2 >> (4 * h)) & 15u;
+            float dq;
+            if (fast) {
+              dq = tq[c & 7];
+              dq = (c & 8u) ? -dq : dq;
+            } else {
+              dq = deq_mbs(c, biased, m8);
+            }
+            const double diff = __dsub_rn((double)dq, (double)v[i + h]);
+            mine[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
+          }
+        }
+      }
+      __syncwarp();
+      double sse = 0.0;
+      if (sub == 0 && live_group) sse = pw_sum_smem(gbase, 0, width);
+      __syncwarp();
+      if (sub == 0) {
+        const bool better = (t == 0) || (sse < best_sse) || (sse == best_sse && m8 < best_m8);
+        if (better) { best_sse = sse; best_m8 = m8; }
+      }
+    }
+    const uint32_t m8 = __shfl_sync(0xffffffffu, best_m8, lane & ~(g.G - 1));
+    uint32_t packed[2];
+    bool ovf;
+    const uint8_t biased = mbs_block(v, mbs_factor(m8), packed, ovf);
+    if (active) {
+      bad |= ovf ? 2u : 0u;
+      store_mbs_outputs(q, r, mac, c0 / 16, packed, biased);
+      if (sub == 0) store_m8(q, r, mac, (uint8_t)m8);
+    }
+  }
+  if (bad & 1u) atomicOr(status, ST_NONFINITE);
+  if (bad & 2u) atomicOr(status, ST_OVERFLOW);
+}
+
+// ---------------------------------------------------------------------------
+// K4: NVFP4.  Pass 1: |x| max over the tensor (uint ordering of non-negative
+// floats), non-finite check.  Pass 2: per-block E4M3 scale from the f64 ratio
+// and f64 element division (f32 division changes 1-2 codes per
+// 16.8M elements).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_absmax(const void* __restrict__ x, int dtype, int64_t x_ld, int64_t rows,
+                                                int64_t cols, uint32_t* __restrict__ status) {
+  const int64_t nbr = cols / 16, nb = rows * nbr;
+  float m = 0.0f;
+  uint32_t bad = 0;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = b / nbr, kb = b - r * nbr;
+    float v[16];
+    load_block<16>(x, dtype, r * x_ld + kb * 16, v);
+    bool fin;
+    m = fmaxf(m, block_absmax<16>(v, fin));
+    bad |= !fin;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (m > 0.0f) atomicMax(status + 1, __float_as_uint(m));
+    if (bad) atomicOr(status, ST_NONFINITE);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_quantize_nvfp4(const void* __restrict__ x, int dtype, int64_t x_ld, QDesc q,
+                                                        const uint32_t* __restrict__ amax_bits) {
+  const float amax = __uint_as_float(*amax_bits);
+  const double st = amax > 0.0f ? (double)amax / 2688.0 : 1.0;
+  const double six_st = 6.0 * st;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && q.tensor_scale) *q.tensor_scale = st;
+  const int64_t nbr = q.cols / 16, nb = q.rows * nbr;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = b / nbr, kb = b - r * nbr;
+    float v[16];
+    load_block<16>(x, dtype, r * x_ld + kb * 16, v);
+    bool fin;
+    const float alpha = block_absmax<16>(v, fin);
+    const uint32_t sb = amax > 0.0f ? e4m3_code_f64((double)alpha / six_st) : 0u;
+    const double den = st * e4m3_decode(sb);
+    uint32_t packed[2] = {0u, 0u};
+    if (den > 0.0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t c = e2m1_code_f64(__ddiv_rn((double)v[i], den));
+        packed[i >> 3] |= c << (4 * (i & 7));
+      }
+    }
+    store_codes<16>(q.codes + r * q.codes_ld + kb * 8, packed);
+    store_scale(q, r, kb, (uint8_t)sb);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K5: dequantise to f32 (src/quantize.py:728-746).  Thread == block.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dequantize(QDesc q, float* __restrict__ out, int64_t out_ld,
+                                                    uint32_t* __restrict__ status) {
+  const int bs = q.block_size;
+  const int64_t nbr = q.cols / bs, nb = q.rows * nbr;
+  const double st = (q.variant == NVFP4 && q.tensor_scale) ? *q.tensor_scale : 1.0;
+  uint32_t bad = 0;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = b / nbr, kb = b - r * nbr;
+    const uint32_t s = q.scales[r * q.scales_ld + kb];
+    uint32_t m8 = 0;
+    if (q.mant) m8 = q.mant[r * q.mant_ld + (kb * bs) / q.macro_size];
+    if (q.variant == NVFP4) bad |= ((s & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
+    else bad |= (s == 255u) ? ST_BAD_E8M0 : 0u;
+    const uint8_t* cp = q.codes + r * q.codes_ld + kb * (bs / 2);
+    float* op = out + r * out_ld + kb * bs;
+    for (int w = 0; w < bs / 8; ++w) {
+      const uint32_t word = *reinterpret_cast<const uint32_t*>(cp + 4 * w);
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t c = (word >> (4 * j)) & 15u;
+        if (q.variant == NVFP4) o[j] = deq_nvfp4(c, s, st);
+        else if (q.mant) o[j] = deq_mbs(c, s, m8);
+        else o[j] = deq_pow2(c, s);
+      }
+      float4* o4 = reinterpret_cast<float4*>(op + 8 * w);
+      __stcs(o4, make_float4(o[0], o[1], o[2], o[3]));
+      __stcs(o4 + 1, make_float4(o[4], o[5], o[6], o[7]));
+    }
+  }
+  if (bad) atomicOr(status, bad);
+}
+
+// ---------------------------------------------------------------------------
+// Host launchers
+// ---------------------------------------------------------------------------
+static int grid_for(int64_t work, int threads) {
+  int64_t g = (work + threads - 1) / threads;
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int macro_lanes(int macro) {
+  int nblk = macro / 16, G = 1;
+  while (G < nblk) G <<= 1;
+  return G;
+}
+
+int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int mbs_mode, const uint8_t* cand,
+                    int n_cand, int augment, uint32_t* status, cudaStream_t st) {
+  const int64_t rows = q.rows, cols = q.cols;
+  switch (q.variant) {
+    case OCP32: {
+      const int64_t nb = rows * (cols / 32);
+      k_quantize_pow2<32, true, false><<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status);
+      break;
+    }
+    case MX16:
+    case MX16_OAS: {
+      const int64_t nb = rows * (cols / 16);
+      if (q.variant == MX16)
+        k_quantize_pow2<16, false, false><<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status);
+      else
+        k_quantize_pow2<16, false, true><<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status);
+      break;
+    }
+    case MBS_S:
+    case MBS_D: {
+      MacroGeom g;
+      g.macro = q.macro_size;
+      g.G = macro_lanes(q.macro_size);
+      g.nmac = (cols + q.macro_size - 1) / q.macro_size;
+      if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
+      const int64_t ngroups = rows * g.nmac;
+      if (q.variant == MBS_S) {
+        k_quantize_mbs_s<<<grid_for(ngroups * g.G, 256), 256, 0, st>>>(x, dtype, x_ld, q, g, status);
+      } else {
+        if (mbs_mode != 0) return set_error(ERR_INVALID, "mbs_mode='lut' runs through mxq_quantize_mbs_lut");
+        if (n_cand < 1 || n_cand > 256) return set_error(ERR_INVALID, "candidate count out of range");
+        cudaError_t e = cudaMemcpyToSymbolAsync(c_cands, cand, (size_t)n_cand, 0, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return set_cuda_error(e);
+        const int64_t gpb = MBSD_THREADS / g.G;
+        int64_t blocks = (ngroups + gpb - 1) / gpb;
+        int64_t cap = (int64_t)num_sms() * 16;
+        k_quantize_mbs_d<false><<<(int)(blocks < cap ? blocks : cap), MBSD_THREADS, 0, st>>>(
+            x, dtype, x_ld, q, g, n_cand, augment, status);
+      }
+      break;
+    }
+    case NVFP4: {
+      const int64_t nb = rows * (cols / 16);
+      cudaError_t e = cudaMemsetAsync(status + 1, 0, sizeof(uint32_t), st);
+      if (e != cudaSuccess) return set_cuda_error(e);
+      k_absmax<<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, rows, cols, status);
+      k_quantize_nvfp4<<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status + 1);
+      break;
+    }
+    default:
+      return set_error(ERR_INVALID, "unknown variant");
+  }
+  return check_launch();
+}
+
+int launch_quantize_lut(const void* x, int dtype, int64_t x_ld, const QDesc& q, const uint8_t* cand, int n_cand,
+                        const float* lut, uint32_t* status, cudaStream_t st) {
+  if (q.variant != MBS_D) return set_error(ERR_INVALID, "lut mode applies to MBS_D only");
+  if (n_cand != 16) return set_error(ERR_INVALID, "the lookup table holds exactly 16 candidates");
+  MacroGeom g;
+  g.macro = q.macro_size;
+  g.G = macro_lanes(q.macro_size);
+  g.nmac = (q.cols + q.macro_size - 1) / q.macro_size;
+  if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_cands, cand, 16, 0, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(c_lut, lut, sizeof(float) * 2 * 16 * 64, 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  const int64_t ngroups = q.rows * g.nmac;
+  const int64_t gpb = MBSD_THREADS / g.G;
+  int64_t blocks = (ngroups + gpb - 1) / gpb;
+  int64_t cap = (int64_t)num_sms() * 16;
+  k_quantize_mbs_d<true><<<(int)(blocks < cap ? blocks : cap), MBSD_THREADS, 0, st>>>(x, dtype, x_ld, q, g, 16, 0,
+                                                                                     status);
+  return check_launch();
+}
+
+int launch_dequantize(const QDesc& q, float* out, int64_t out_ld, uint32_t* status, cudaStream_t st) {
+  const int64_t nb = q.rows * (q.cols / q.block_size);
+  k_dequantize<<<grid_for(nb, 256), 256, 0, st>>>(q, out, out_ld, status);
+  return check_launch();
+}
+
+}  // namespace mxq

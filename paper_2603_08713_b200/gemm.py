@@ -1,0 +1,156 @@
+"""Quantized GEMM on the B200 (drop-in for src/gemm.py).
+
+``matmul_quantized`` runs the tcgen05 block-scaled kernel (csrc/gemm_tc.cu)
+for every operand pair the tensor cores can take natively (any two
+E8M0-scaled variants, NVFP4 x NVFP4), applying the MBS factor per 128-K macro
+chunk in the epilogue; its output matches the reference dequantize-then-f64
+matmul within the tolerance stated in DESIGN.md.  ``exact=True`` (and the
+E8M0 x E4M3 pairs, which have no single block-scaled MMA form) use the
+CUDA-core f64 kernel (csrc/gemm_exact.cu), which is bit-identical to the
+reference's ``matmul_quantized`` / ``matmul_reference``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .quantize import QuantizedTensor, Variant
+
+__all__ = ["TileConfig", "OverheadReport", "matmul_reference", "matmul_quantized", "roofline_overhead",
+           "max_ulp_divergence", "tc_supported"]
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Output tile (t_m x t_n) and k-chunk t_k (src/gemm.py:33-43).  Tiles
+    never change results; t_k is validated exactly like the reference and
+    otherwise unused (the kernels chunk K at the macro size)."""
+
+    t_m: int = 128
+    t_n: int = 128
+    t_k: int = 128
+
+    def __post_init__(self) -> None:
+        if self.t_m <= 0 or self.t_n <= 0 or self.t_k <= 0:
+            raise ValueError(f"tile dims must be positive, got {self}")
+
+
+@dataclass(frozen=True)
+class OverheadReport:
+    compute_ratio: float
+    traffic_ratio: float
+
+
+def _dense_f32(t, name: str) -> torch.Tensor:
+    dev = _lib.require_device()
+    x = t if isinstance(t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32))
+    x = x.to(device=dev, dtype=torch.float32)
+    if x.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got shape {tuple(x.shape)}")
+    return x.contiguous()
+
+
+def matmul_reference(a, b) -> torch.Tensor:
+    """C = A @ B.T with f64 products summed in ascending k, one f32 rounding
+    (src/gemm.py:68-90), on CUDA cores; bit-identical to the reference."""
+    a32, b32 = _dense_f32(a, "a"), _dense_f32(b, "b")
+    if a32.shape[1] != b32.shape[1]:
+        raise ValueError(f"inner dimensions differ: {tuple(a32.shape)} vs {tuple(b32.shape)}")
+    m, k = a32.shape
+    n = b32.shape[0]
+    c = torch.empty((m, n), dtype=torch.float32, device=a32.device)
+    _lib.check(_lib.lib().mxq_matmul_reference(a32.data_ptr(), k, b32.data_ptr(), k, m, n, k, c.data_ptr(), n,
+                                               _lib.stream_handle()), "matmul_reference")
+    return c
+
+
+def _validate_chunking(q: QuantizedTensor, t_k: int, name: str) -> None:
+    """src/gemm.py:126-134."""
+    if t_k % q.block_size != 0:
+        raise ValueError(f"t_k {t_k} is not a multiple of operand {name}'s block size {q.block_size}")
+    if q.mbs_mantissas is not None and t_k % q.macro_size != 0:
+        raise ValueError(f"t_k {t_k} is not a multiple of operand {name}'s macro size {q.macro_size}")
+
+
+def tc_supported(aq: QuantizedTensor, bq: QuantizedTensor) -> bool:
+    """Whether the pair runs on the tcgen05 block-scaled path."""
+    nva, nvb = aq.variant is Variant.NVFP4, bq.variant is Variant.NVFP4
+    if nva != nvb:
+        return False  # UE8M0 x UE4M3: no single MMA scale format
+    for q in (aq, bq):
+        if q.mbs_mantissas is not None and q.macro_size % 64:
+            return False  # sigma chunks must align with the 64-K MMA step
+    if aq.mbs_mantissas is not None and bq.mbs_mantissas is not None and aq.macro_size != bq.macro_size:
+        return False
+    return True
+
+
+def _sf_block(aq: QuantizedTensor, bq: QuantizedTensor) -> int:
+    return 32 if (aq.block_size == 32 and bq.block_size == 32) else 16
+
+
+def matmul_quantized(aq: QuantizedTensor, bq: QuantizedTensor, cfg: TileConfig = TileConfig(), *,
+                     exact: bool = False, out_dtype: torch.dtype = torch.float32, out: torch.Tensor = None,
+                     check: bool = True) -> torch.Tensor:
+    """C = dequant(aq) @ dequant(bq).T (src/gemm.py:137-172) as a CUDA tensor.
+
+    Operand variants may be mixed (e.g. MBS-H = MBS_S activations x MBS_D
+    weights).  ``exact=True`` gives the reference's bit-exact f64 result.
+    """
+    if aq.shape[1] != bq.shape[1]:
+        raise ValueError(f"operands disagree on K: {aq.shape} vs {bq.shape}")
+    _validate_chunking(aq, cfg.t_k, "a")
+    _validate_chunking(bq, cfg.t_k, "b")
+    m, n = aq.shape[0], bq.shape[0]
+    dev = aq.codes.device
+    status = torch.zeros(4, dtype=torch.int32, device=dev)
+    stream = _lib.stream_handle()
+    L = _lib.lib()
+    if exact or not tc_supported(aq, bq):
+        c = torch.empty((m, n), dtype=torch.float32, device=dev)
+        qa, qb = aq.qt(), bq.qt()
+        _lib.check(L.mxq_gemm_exact(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), n, status.data_ptr(), stream),
+                   "matmul_quantized(exact)")
+        if check:
+            _lib.raise_on_status(status)
+        return c if out_dtype == torch.float32 else c.to(out_dtype)
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("out_dtype must be float32 or bfloat16")
+    c = out if out is not None else torch.empty((m, n), dtype=out_dtype, device=dev)
+    sfb = _sf_block(aq, bq)
+    qa, qb = aq.gemm_qt(sfb), bq.gemm_qt(sfb)
+    dt = _lib.MXQ_BF16 if out_dtype == torch.bfloat16 else _lib.MXQ_F32
+    _lib.check(L.mxq_gemm(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), dt, c.stride(0), status.data_ptr(),
+                          stream), "matmul_quantized")
+    return c
+
+
+def roofline_overhead(cfg: TileConfig, sigma_bytes: int = 2, out_bytes: int = 4) -> OverheadReport:
+    """Per-chunk scale-application cost vs the 4-bit tensor work
+    (src/gemm.py:175-193, Appendix B)."""
+    if sigma_bytes <= 0 or out_bytes <= 0:
+        raise ValueError("byte widths must be positive")
+    return OverheadReport(compute_ratio=2.0 / cfg.t_k,
+                          traffic_ratio=((cfg.t_m + cfg.t_n) * sigma_bytes) / (cfg.t_m * cfg.t_n * out_bytes))
+
+
+def max_ulp_divergence(a, b) -> int:
+    """Largest ulp distance between two float32 arrays (src/gemm.py:196-214)."""
+    to_np = lambda t: t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else t
+    x = np.ascontiguousarray(to_np(a), dtype=np.float32)
+    y = np.ascontiguousarray(to_np(b), dtype=np.float32)
+    if x.shape != y.shape:
+        raise ValueError(f"shape mismatch: {x.shape} vs {y.shape}")
+    if x.size == 0:
+        return 0
+
+    def key(v: np.ndarray) -> np.ndarray:
+        bits = v.view(np.uint32).astype(np.int64)
+        return np.where(bits & 0x80000000, 0x80000000 - bits, bits)
+
+    return int(np.max(np.abs(key(x) - key(y))))

@@ -1,0 +1,220 @@
+"""GPU parity: the sm_100a quantizers, dequantiser and evaluator against the
+reference's golden outputs (tests/golden/) and the CPU oracle.
+
+Bit-exact: codes, E8M0 / E4M3 scales, MBS mantissas, NVFP4 tensor scale,
+dequantised f32 values, QSNR (mse / signal f64 sums) and flush rates.
+"""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import mxq_oracle as O
+from tests._cases import CONFIGS, golden_cases
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_08713_b200 as M  # noqa: E402
+
+
+def _cfg(cname):
+    variant, kw = CONFIGS[cname]
+    kw = dict(kw)
+    if "candidates" in kw:
+        kw["candidates"] = M.CandidateSet(tuple(kw["candidates"]))
+    return M.SchemeConfig(M.Variant(variant), **kw)
+
+
+def _np(t):
+    return None if t is None else t.cpu().numpy()
+
+
+def _assert_q_equal(q, want, key):
+    for f in ("codes", "block_scales", "e4m3_scales", "mbs_mantissas"):
+        w = want.get(f)
+        g = _np(getattr(q, f))
+        assert (w is None) == (g is None), (key, f)
+        if w is not None:
+            assert np.array_equal(g, w), (key, f, int(np.sum(g != w)))
+    if want.get("tensor_scale") is not None:
+        assert float(q.tensor_scale) == float(want["tensor_scale"]), key
+
+
+def _golden_q(golden, key):
+    out = {}
+    for f in ("codes", "block_scales", "e4m3_scales", "mbs_mantissas", "tensor_scale"):
+        k = f"{key}/{f}"
+        if k in golden.files:
+            out[f] = golden[k] if f != "tensor_scale" else float(golden[k][0])
+    return out
+
+
+def test_device_is_b200():
+    assert torch.cuda.is_available()
+    assert torch.cuda.get_device_capability()[0] == 10
+    assert M._lib.lib().mxq_device_ok() == 1
+
+
+def test_quantize_dequantize_match_golden(golden):
+    n = 0
+    for tname, cname in golden_cases(golden):
+        t = golden[f"in/{tname}"]
+        key = f"q/{tname}/{cname}"
+        q = M.quantize_tensor(t, _cfg(cname))
+        _assert_q_equal(q, _golden_q(golden, key), key)
+        deq = M.dequantize_tensor(q).cpu().numpy()
+        assert np.array_equal(deq.view(np.uint32), golden[f"{key}/deq"].view(np.uint32)), key
+        n += 1
+    assert n > 100
+
+
+def test_bf16_input_matches_f32_input(golden):
+    t = golden["in/bf16_gwo_64x512"]  # already bf16-representable
+    tb = torch.from_numpy(t).cuda().to(torch.bfloat16)
+    for cname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4"):
+        assert M.quantize_tensor(tb, _cfg(cname)) == M.quantize_tensor(t, _cfg(cname)), cname
+
+
+def test_qsnr_and_flush_match_golden(golden, golden_meta):
+    for rec in golden_meta["cases"]:
+        t = golden[f"in/{rec['tensor']}"]
+        q = M.quantize_tensor(t, _cfg(rec["config"]))
+        assert M.flush_to_zero_rate(t, q) == rec["flush"], rec
+        if "qsnr_db" not in rec:
+            continue
+        rep = M.qsnr_tensor(t, M.dequantize_tensor(q))
+        rep2, fl2 = M.qsnr_quantized(t, q)
+        for r in (rep, rep2):
+            assert r.mse == rec["mse"] and r.signal_power == rec["signal"], rec
+            want = rec["qsnr_db"]
+            assert (r.qsnr_db == want) or (math.isinf(r.qsnr_db) and math.isinf(float(want))), rec
+        assert fl2 == rec["flush"]
+
+
+def test_qsnr_kats():
+    rng = np.random.Generator(np.random.PCG64(201))
+    ref = rng.standard_normal((8, 32)).astype(np.float32)
+    assert M.qsnr_tensor(ref, ref).qsnr_db == math.inf
+    assert M.qsnr_tensor(ref, np.zeros_like(ref)).qsnr_db == pytest.approx(0.0, abs=1e-12)
+    assert M.qsnr_tensor(ref, ref / 2).qsnr_db == pytest.approx(10 * math.log10(4.0), abs=1e-9)
+    with pytest.raises(ValueError):
+        M.qsnr_tensor(np.zeros((2, 8), np.float32), np.ones((2, 8), np.float32))
+    with pytest.raises(ValueError):
+        M.qsnr_tensor(ref, ref[:, :16])
+
+
+def test_e2m1_hardware_conversion_kat():
+    """cvt.rn.satfinite.e2m1x2.f32 + the -0 fix against the reference encoder
+    on every midpoint, its f32 neighbours, tiny values, saturation and both
+    nibble orders."""
+    mids = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0], np.float32)
+    vals = np.concatenate([mids, np.nextafter(mids, np.float32(0)), np.nextafter(mids, np.float32(9)),
+                           np.float32([0.0, 1e-30, 6.0, 6.6, 7.5, 5.99, 0.1, 2.0, 3.0, 4.0])])
+    vals = np.concatenate([vals, -vals]).astype(np.float32)
+    per = 30  # 30 values + two pins per 32-block
+    nb = -(-vals.size // per)
+    blocks = np.zeros((nb, 32), np.float32)
+    blocks[:, :per].flat[: vals.size] = vals
+    blocks[:, -1] = 4.0  # OCP32: alpha in [4, 8) -> D = 1, so codes = encode(x)
+    blocks[:, -2] = -4.0
+    t = blocks.reshape(1, -1)
+    q = M.quantize_tensor(t, M.SchemeConfig(M.Variant.OCP32))
+    assert np.all(_np(q.block_scales) == 127)
+    got = _np(q.unpack_codes())[0]
+    want = O.e2m1_encode(t[0].astype(np.float64))
+    assert np.array_equal(got, want)
+
+
+def test_nonfinite_and_corrupt_scales_raise():
+    t = np.ones((2, 32), np.float32)
+    t[1, 3] = np.inf
+    for v in M.Variant:
+        with pytest.raises(ValueError, match="non-finite"):
+            M.quantize_tensor(t, M.SchemeConfig(v))
+    q = M.quantize_tensor(np.ones((2, 32), np.float32), M.SchemeConfig(M.Variant.MX16))
+    bad = q.block_scales.clone()
+    bad[0, 0] = 255
+    import dataclasses
+    with pytest.raises(ValueError):
+        M.dequantize_tensor(dataclasses.replace(q, block_scales=bad))
+    with pytest.raises(ValueError):
+        M.quantize_tensor(np.zeros((4, 20), np.float32), M.SchemeConfig(M.Variant.MX16))
+    with pytest.raises(ValueError):
+        M.quantize_tensor(np.zeros(16, np.float32), M.SchemeConfig(M.Variant.MX16))
+
+
+def test_row_partition_and_launch_invariance():
+    """tests/test_quantize.py:371-387 plus repeated runs: bit-identical."""
+    rng = np.random.Generator(np.random.PCG64(43))
+    t = rng.standard_t(4, (12, 512)).astype(np.float32)
+    for v in M.Variant:
+        if v is M.Variant.NVFP4:
+            continue
+        cfg = M.SchemeConfig(v)
+        full = M.quantize_tensor(t, cfg)
+        a, b = M.quantize_tensor(t[:5], cfg), M.quantize_tensor(t[5:], cfg)
+        assert torch.equal(full.codes, torch.cat([a.codes, b.codes]))
+        assert torch.equal(full.block_scales, torch.cat([a.block_scales, b.block_scales]))
+        if full.mbs_mantissas is not None:
+            assert torch.equal(full.mbs_mantissas, torch.cat([a.mbs_mantissas, b.mbs_mantissas]))
+        assert full == M.quantize_tensor(t, cfg)
+
+
+def test_mbs_d_matches_oracle_on_random_macros():
+    """Criterion 5 (tests/test_acceptance.py:148-168) on the GPU path."""
+    rng = np.random.Generator(np.random.PCG64(55))
+    macros = np.concatenate([
+        rng.standard_normal((2000, 128)), rng.standard_t(4, (2000, 128)),
+        np.where(rng.random((1000, 128)) < 0.01, rng.standard_normal((1000, 128)) * 100,
+                 rng.standard_normal((1000, 128)))]).astype(np.float32)
+    q = M.quantize_tensor(macros, M.SchemeConfig(M.Variant.MBS_D))
+    want = O.choose_exact(macros, tuple(range(0, 256, 16)), True)
+    assert np.array_equal(_np(q.mbs_mantissas).ravel(), want)
+
+
+@pytest.mark.parametrize("variant", ["ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4"])
+def test_config1_full_size_bit_exact(golden_meta, variant):
+    """Config 1 (4096x4096 bf16 gaussian+outliers, seed 0): the GPU output
+    digest and QSNR equal the reference's (computed in the build container
+    by tests/golden/make_golden.py)."""
+    t = O.bf16_round(O.generate("gaussian_with_outliers", (4096, 4096), 0))
+    assert hashlib.sha256(t.tobytes()).hexdigest() == golden_meta["config1_sha256_bf16"]
+    tb = torch.from_numpy(t).cuda().to(torch.bfloat16)
+    q = M.quantize_tensor(tb, M.SchemeConfig(M.Variant(variant)))
+    h = hashlib.sha256()
+    fields = {"codes": q.codes, "block_scales": q.block_scales, "e4m3_scales": q.e4m3_scales,
+              "mbs_mantissas": q.mbs_mantissas}
+    if q.tensor_scale is not None:
+        fields["tensor_scale"] = np.array([q.tensor_scale], np.float64)
+    for f in sorted(k for k, v in fields.items() if v is not None):
+        v = fields[f]
+        h.update(f.encode())
+        h.update(np.ascontiguousarray(v.cpu().numpy() if isinstance(v, torch.Tensor) else v).tobytes())
+    want = golden_meta["config1"][variant]
+    assert h.hexdigest() == want["sha256"]
+    rep, fl = M.qsnr_quantized(tb, q)
+    assert rep.qsnr_db == want["qsnr_db"] and rep.mse == want["mse"] and rep.signal_power == want["signal"]
+    assert fl == want["flush"]
+
+
+def test_exact_gemm_matches_golden(golden, golden_meta):
+    from tests._cases import split_pair
+    a, b = golden["gemm/a"], golden["gemm/b"]
+    for pair in golden_meta["gemm_pairs"]:
+        va, vb = split_pair(pair)
+        aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant(va)))
+        bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant(vb)))
+        c = M.matmul_quantized(aq, bq, M.TileConfig(16, 8, 128), exact=True).cpu().numpy()
+        assert np.array_equal(c, golden[f"gemm/{pair}"]), pair
+
+
+def test_matmul_reference_exact():
+    rng = np.random.Generator(np.random.PCG64(101))
+    a = rng.standard_normal((24, 96)).astype(np.float32)
+    b = rng.standard_normal((17, 96)).astype(np.float32)
+    assert np.array_equal(M.matmul_reference(a, b).cpu().numpy(), O.matmul_ref(a, b))
+    one = M.matmul_reference(np.array([[2.0, 3.0]], np.float32), np.array([[4.0, 5.0]], np.float32))
+    assert float(one[0, 0]) == 23.0

@@ -1,0 +1,80 @@
+"""Pin the CPU oracle (oracle/mxq_oracle.py) to the real reference's outputs.
+
+The fixtures in tests/golden/ were produced by running /root/reference's own
+`mxq` package (tests/golden/make_golden.py).  Every oracle function used as a
+checker for the CUDA path is compared bit-for-bit here.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import mxq_oracle as O
+from tests._cases import CONFIGS, golden_cases, split_pair
+
+
+def test_e2m1_codec_matches_reference(golden):
+    got = O.e2m1_encode(golden["codec/e2m1_in"])
+    assert np.array_equal(got, golden["codec/e2m1_out"])
+
+
+def test_e4m3_codec_matches_reference(golden):
+    assert np.array_equal(O.E4M3, golden["codec/e4m3_table"], equal_nan=True)
+    got = O.e4m3_encode(golden["codec/e4m3_in"])
+    assert np.array_equal(got, golden["codec/e4m3_out"])
+
+
+def test_quantizers_match_reference(golden):
+    n = 0
+    for tname, cname in golden_cases(golden):
+        variant, kw = CONFIGS[cname]
+        t = golden[f"in/{tname}"]
+        q = O.quantize(t, variant, **kw)
+        key = f"q/{tname}/{cname}"
+        for f in ("codes", "block_scales", "e4m3_scales", "mbs_mantissas"):
+            want = golden[f"{key}/{f}"] if f"{key}/{f}" in golden.files else None
+            got = getattr(q, f)
+            assert (want is None) == (got is None), (key, f)
+            if want is not None:
+                assert np.array_equal(got, want), (key, f)
+        if f"{key}/tensor_scale" in golden.files:
+            assert q.tensor_scale == float(golden[f"{key}/tensor_scale"][0]), key
+        deq = O.dequantize(q)
+        assert np.array_equal(deq.view(np.uint32), golden[f"{key}/deq"].view(np.uint32)), key
+        n += 1
+    assert n > 100
+
+
+def test_qsnr_and_flush_match_reference(golden, golden_meta):
+    for rec in golden_meta["cases"]:
+        variant, kw = CONFIGS[rec["config"]]
+        t = golden[f"in/{rec['tensor']}"]
+        q = O.quantize(t, variant, **kw)
+        assert O.flush_rate(t, q) == rec["flush"]
+        if "qsnr_db" in rec:
+            db, mse, sig = O.qsnr(t, O.dequantize(q))
+            assert (db == rec["qsnr_db"]) or (math.isinf(db) and rec["qsnr_db"] is None) or \
+                (math.isinf(db) and math.isinf(float(rec["qsnr_db"])))
+            assert mse == rec["mse"] and sig == rec["signal"]
+
+
+def test_gemm_matches_reference(golden, golden_meta):
+    a, b = golden["gemm/a"], golden["gemm/b"]
+    for pair in golden_meta["gemm_pairs"]:
+        va, vb = split_pair(pair)
+        c = O.matmul_quantized(O.quantize(a, va), O.quantize(b, vb))
+        assert np.array_equal(c, golden[f"gemm/{pair}"]), pair
+
+
+def test_ulp_distance():
+    x = np.array([1.0, -2.5, 0.0], np.float32)
+    assert O.ulp_distance(x, x) == 0
+    assert O.ulp_distance(x, np.nextafter(x, np.float32(np.inf))) == 1
+    assert O.ulp_distance(np.array([0.0], np.float32), np.array([-0.0], np.float32)) == 0
+
+
+def test_generator_reproduces_config1_digest(golden_meta):
+    import hashlib
+    t = O.bf16_round(O.generate("gaussian_with_outliers", (4096, 4096), 0))
+    assert hashlib.sha256(t.tobytes()).hexdigest() == golden_meta["config1_sha256_bf16"]
