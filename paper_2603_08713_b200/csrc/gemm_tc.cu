@@ -1,12 +1,571 @@
-// gemm_tc.cu -- tcgen05 block-scaled GEMM (K7-K9).  Placeholder until the
-// kernel lands; the C-ABI reports the path as unsupported.
+// gemm_tc.cu -- tcgen05 block-scaled FP4 GEMM for sm_100a (K7 plain MXFP4,
+// K8 MBS, K9 NVFP4).   C[M,N] = A[M,K] . B[N,K]^T
+//
+// Replaces matmul_quantized (src/gemm.py:137-172).  The reference decodes
+// every element to f32 (g*D/f*s_t) and accumulates f64 products; here the
+// 5th-gen tensor core consumes the packed E2M1 codes and the per-block scale
+// factors directly (kind::mxf4 block32 for OCP32 x OCP32, kind::mxf4nvf4
+// block16 with UE8M0 or UE4M3 scales otherwise) and accumulates in f32 in
+// TMEM.  The MBS factor sigma = 1/(1+m8/256) is per (row, 128-K macro) of each
+// operand, so it cannot ride in the power-of-two block scales: every macro
+// chunk is MMA'd into its own TMEM partial buffer and the epilogue warps fold
+// acc += sigmaA[i,t] * sigmaB[j,t] * P[i,j] in registers (the paper's
+// Appendix E scheme; per-chunk semantics SPEC.md:325).
+//
+// Structure (persistent, one CTA per SM, warp-specialised, cta_group::1):
+//   warp 0        TMA producer: A/B code tiles (2-D TMA, 128B swizzle) and the
+//                 scale-factor atoms (1-D bulk copies) into a STAGES-deep ring
+//   warp 1        TMEM allocator + single-thread MMA issuer: tcgen05.cp of the
+//                 scale atoms smem->TMEM, then tcgen05.mma per 64-K step
+//   warps 4..11   epilogue: tcgen05.ld of the accumulator (plain) or of each
+//                 chunk's partial (MBS), sigma / s_t scaling, f32|bf16 stores
+//
+// Tile 128 x BN, K stage = 256 elements (128 bytes of codes per row).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "mxq_arith.cuh"
 #include "mxq_internal.h"
 
 namespace mxq {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int KSTAGE = 256;            // elements per pipeline stage
+constexpr int KSTEP = 64;              // elements per tcgen05.mma (FP4, K64)
+constexpr int STAGE_BYTES_A = BM * KSTAGE / 2;  // 16 KB
+constexpr int NUM_THREADS = 384;       // 4 control warps + 8 epilogue warps
+constexpr int EPI_WARP0 = 4;
+constexpr int NUM_EPI_WARPS = 8;
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
+// start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48),
+// base offset [49,52), layout [61,64) (2 = 128B swizzle, 0 = none).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7u) << 61;
+  return d;
+}
+
+// K-major operand tile, 128-byte rows with the 128B swizzle, 8-row groups
+// 1024 bytes apart.  Advancing K inside the swizzle atom = start + bytes.
+__device__ __forceinline__ uint64_t operand_desc(uint32_t saddr) { return smem_desc(saddr, 16, 1024, 2); }
+
+// Scale-factor atom (32 rows x 16 B, 8-row core matrices 128 B apart).
+__device__ __forceinline__ uint64_t sf_desc(uint32_t saddr) { return smem_desc(saddr, 0, 128, 0); }
+
+__device__ __forceinline__ void utccp_sf(uint32_t tmem_col, uint64_t desc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem_col), "l"(desc) : "memory");
+}
+
+template <bool SF32>
+__device__ __forceinline__ void mma_bs(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum, uint32_t sfa, uint32_t sfb) {
+  if constexpr (SF32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
+        : "memory");
+  }
+}
+
+// 32 lanes x 32 consecutive 32-bit TMEM columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low half)
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ void epi_bar_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Kernel parameters
+// ---------------------------------------------------------------------------
+struct Params {
+  const uint8_t* sfa;   // scale-factor atoms, [M/128][kgroups][512]
+  const uint8_t* sfb;
+  int64_t sfa_kg, sfb_kg;  // 4-block groups per 128-row block (sf_kpad / 4)
+  const uint8_t* mta;   // transposed mantissas (n_macros, ld) or null
+  const uint8_t* mtb;
+  int64_t mta_ld, mtb_ld;
+  const double* tsa;    // NVFP4 tensor scales or null
+  const double* tsb;
+  void* c;
+  int64_t ldc;
+  int M, N, K;
+  int macro_steps;      // MBS chunk length in 64-K MMA steps
+  int n_chunks;         // MBS chunks per tile (== n_macros)
+  uint32_t idesc;       // instruction descriptor without scale-factor ids
+};
+
+template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
+struct Cfg {
+  static constexpr int STAGE_BYTES_B = BN * KSTAGE / 2;
+  static constexpr int SF_ATOMS_PER_STAGE = SF32 ? 2 : 4;  // 512-B atoms per 128 rows per stage
+  static constexpr int SFA_BYTES = SF_ATOMS_PER_STAGE * 512;
+  static constexpr int SFB_BYTES = SF_ATOMS_PER_STAGE * 512 * (BN / 128);
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * STAGE_BYTES_A;
+  static constexpr int OFF_SFA = OFF_B + STAGES * STAGE_BYTES_B;
+  static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
+  static constexpr int OFF_SIGB = OFF_SFB + STAGES * SFB_BYTES;       // MBS: 2 x BN floats
+  static constexpr int OFF_BAR = OFF_SIGB + (MBS ? 2 * BN * 4 : 0);
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
+  static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
+  // TMEM columns: NB accumulators of BN columns, then 2 parity sets of SF.
+  static constexpr int SFA_COLS = SF_ATOMS_PER_STAGE * 4;
+  static constexpr int SFB_COLS = SF_ATOMS_PER_STAGE * 4 * (BN / 128);
+  static constexpr int COL_SF = NB * BN;
+  static constexpr int TMEM_COLS_USED = COL_SF + 2 * (SFA_COLS + SFB_COLS);
+  static constexpr int TMEM_COLS = 512;
+  static_assert(TMEM_COLS_USED <= 512, "TMEM budget");
+  static_assert(SMEM <= 232448, "shared memory budget");
+};
+
+template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + NB;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + NB);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int n_stages = (p.K + KSTAGE - 1) / KSTAGE;
+  const int n_ksteps = (p.K + KSTEP - 1) / KSTEP;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], NUM_EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int mb = tile % tiles_m, nb = tile / tiles_m;
+        const int m0 = mb * BM, n0 = nb * BN;
+        for (int s = 0; s < n_stages; ++s) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::TX_BYTES);
+          tma_load_2d(smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, &full[stage], s * (KSTAGE / 2), m0);
+          tma_load_2d(smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, &full[stage], s * (KSTAGE / 2), n0);
+          const uint8_t* sa = p.sfa + ((int64_t)mb * p.sfa_kg + (int64_t)s * C::SF_ATOMS_PER_STAGE) * 512;
+          bulk_load(smem + C::OFF_SFA + stage * C::SFA_BYTES, sa, C::SFA_BYTES, &full[stage]);
+#pragma unroll
+          for (int rb = 0; rb < BN / 128; ++rb) {
+            const uint8_t* sb =
+                p.sfb + ((int64_t)(n0 / 128 + rb) * p.sfb_kg + (int64_t)s * C::SF_ATOMS_PER_STAGE) * 512;
+            bulk_load(smem + C::OFF_SFB + stage * C::SFB_BYTES + rb * C::SF_ATOMS_PER_STAGE * 512, sb,
+                      C::SF_ATOMS_PER_STAGE * 512, &full[stage]);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t chunk_ctr = 0;  // accumulator buffers used so far
+      uint32_t sf_par = 0;
+      const int chunk_len = MBS ? p.macro_steps : (1 << 30);
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int kstep = 0;
+        uint32_t buf = 0;
+        bool open = false;
+        for (int s = 0; s < n_stages; ++s) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          // scale factors of this stage: smem -> TMEM (parity-buffered)
+          const uint32_t sfa_col = tmem + C::COL_SF + sf_par * (C::SFA_COLS + C::SFB_COLS);
+          const uint32_t sfb_col = sfa_col + C::SFA_COLS;
+          const uint32_t sfa_s = smem_u32(smem + C::OFF_SFA + stage * C::SFA_BYTES);
+          const uint32_t sfb_s = smem_u32(smem + C::OFF_SFB + stage * C::SFB_BYTES);
+#pragma unroll
+          for (int a = 0; a < C::SF_ATOMS_PER_STAGE; ++a) {
+            utccp_sf(sfa_col + a * 4, sf_desc(sfa_s + a * 512));
+#pragma unroll
+            for (int rb = 0; rb < BN / 128; ++rb)
+              utccp_sf(sfb_col + a * 4 * (BN / 128) + rb * 4,
+                       sf_desc(sfb_s + rb * C::SF_ATOMS_PER_STAGE * 512 + a * 512));
+          }
+          const uint32_t a_s = smem_u32(smem + C::OFF_A + stage * STAGE_BYTES_A);
+          const uint32_t b_s = smem_u32(smem + C::OFF_B + stage * C::STAGE_BYTES_B);
+#pragma unroll
+          for (int k = 0; k < KSTAGE / KSTEP; ++k) {
+            if (kstep < n_ksteps) {
+              const int in_chunk = kstep % chunk_len;
+              if (in_chunk == 0) {
+                if (open) tc_commit(&tfull[buf]);
+                buf = chunk_ctr % NB;
+                mbar_wait(&tempty[buf], ((chunk_ctr / NB) & 1) ^ 1);
+                tc_fence_after();
+                ++chunk_ctr;
+                open = true;
+              }
+              uint32_t idesc = p.idesc;
+              int atom = k;
+              if constexpr (SF32) {
+                atom = k >> 1;
+                const uint32_t sf_id = (uint32_t)(k & 1) * 2u;
+                idesc |= (sf_id << 29) | (sf_id << 4);
+              }
+              mma_bs<SF32>(tmem + buf * BN, operand_desc(a_s + k * 32), operand_desc(b_s + k * 32), idesc,
+                           in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
+            }
+            ++kstep;
+          }
+          tc_commit(&empty[stage]);
+          sf_par ^= 1;
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (open) tc_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ===================== epilogue =====================
+    const int e = warp - EPI_WARP0;        // 0..7
+    const int quad = warp & 3;             // TMEM lane quadrant this warp may access
+    const int half = e >> 2;               // column half
+    constexpr int COLS = BN / 2;           // columns per thread
+    const int row_in_tile = quad * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    uint32_t chunk_ctr = 0;
+    float scale_nv = 1.0f;
+    if (p.tsa && p.tsb) scale_nv = (float)(*p.tsa * *p.tsb);
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int mb = tile % tiles_m, nb = tile / tiles_m;
+      const int m0 = mb * BM, n0 = nb * BN;
+      const int row = m0 + row_in_tile;
+      float acc[COLS];
+      if constexpr (!MBS) {
+        const uint32_t buf = chunk_ctr % NB;
+        mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < COLS; c += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_addr + buf * BN + half * COLS + c, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c + i] = v[i] * scale_nv;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        ++chunk_ctr;
+      } else {
+#pragma unroll
+        for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
+        float* sigb = reinterpret_cast<float*>(smem + C::OFF_SIGB);
+        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..255
+        for (int t = 0; t < p.n_chunks; ++t) {
+          // sigma_B for this chunk's BN columns -> shared (parity buffer)
+          if (et < BN) {
+            float sb = 1.0f;
+            if (p.mtb) sb = 1.0f / mbs_factor(p.mtb[(int64_t)t * p.mtb_ld + n0 + et]);
+            sigb[(t & 1) * BN + et] = sb;
+          }
+          float sa = 1.0f;
+          if (p.mta) sa = 1.0f / mbs_factor(p.mta[(int64_t)t * p.mta_ld + m0 + row_in_tile]);
+          epi_bar_sync();
+          const float* sbp = sigb + (t & 1) * BN + half * COLS;
+          const uint32_t buf = chunk_ctr % NB;
+          mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < COLS; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + buf * BN + half * COLS + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[c + i] = fmaf(sa * sbp[c + i], v[i], acc[c + i]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);
+          ++chunk_ctr;
+        }
+      }
+      // ---- store ----
+      if (row < p.M) {
+        const int col0 = n0 + half * COLS;
+        if constexpr (OUT_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
+          if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
+#pragma unroll
+            for (int c = 0; c < COLS; c += 8) {
+              uint4 w;
+              w.x = pack_bf16x2(acc[c + 0], acc[c + 1]);
+              w.y = pack_bf16x2(acc[c + 2], acc[c + 3]);
+              w.z = pack_bf16x2(acc[c + 4], acc[c + 5]);
+              w.w = pack_bf16x2(acc[c + 6], acc[c + 7]);
+              *reinterpret_cast<uint4*>(out + c) = w;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < COLS; ++c)
+              if (col0 + c < p.N) out[c] = __float2bfloat16_rn(acc[c]);
+          }
+        } else {
+          float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col0;
+          if (col0 + COLS <= p.N && (p.ldc % 4) == 0) {
+#pragma unroll
+            for (int c = 0; c < COLS; c += 4)
+              *reinterpret_cast<float4*>(out + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < COLS; ++c)
+              if (col0 + c < p.N) out[c] = acc[c];
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D map over packed codes: inner dim = K/2 bytes, outer = rows; box =
+// 128 bytes x box_rows, 128B swizzle; out-of-bounds reads fill zeros.
+static int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t kbytes, int64_t ld,
+                         int box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return set_error(ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  if ((uintptr_t)base % 16 || ld % 16) return set_error(ERR_INVALID, "codes must be 16-byte aligned with a 16-byte pitch");
+  cuuint64_t dims[2] = {(cuuint64_t)kbytes, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld};
+  cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ERR_INVALID, "cuTensorMapEncodeTiled failed");
+  return 0;
+}
+
+// Block-scaled instruction descriptor (see CUTLASS cute/arch/mma_sm100_desc.hpp
+// InstrDescriptorBlockScaled): a/b format E2M1 = 1 at [7,10)/[10,13), K-major,
+// N>>3 at [17,23), scale format at 23 (1 = UE8M0, 0 = UE4M3), M>>4 at [24,29).
+static uint32_t make_idesc(int n, bool ue8m0) {
+  uint32_t d = 0;
+  d |= 1u << 7;
+  d |= 1u << 10;
+  d |= (uint32_t)(n >> 3) << 17;
+  d |= (ue8m0 ? 1u : 0u) << 23;
+  d |= (uint32_t)(BM >> 4) << 24;
+  return d;
+}
+
+template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
+static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, bool ue8m0, cudaStream_t st) {
+  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
+  auto kern = k_gemm_tc<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  int rc = make_code_map(&ta, a.codes, a.rows, a.cols / 2, a.codes_ld, BM);
+  if (rc) return rc;
+  rc = make_code_map(&tb, b.codes, b.rows, b.cols / 2, b.codes_ld, BN);
+  if (rc) return rc;
+  Params p{};
+  p.sfa = a.scales_mma;
+  p.sfb = b.scales_mma;
+  p.sfa_kg = a.sf_kpad / 4;
+  p.sfb_kg = b.sf_kpad / 4;
+  p.mta = (MBS && a.mant_t) ? a.mant_t : nullptr;
+  p.mtb = (MBS && b.mant_t) ? b.mant_t : nullptr;
+  p.mta_ld = a.mant_t_ld;
+  p.mtb_ld = b.mant_t_ld;
+  p.tsa = a.variant == NVFP4 ? a.tensor_scale : nullptr;
+  p.tsb = b.variant == NVFP4 ? b.tensor_scale : nullptr;
+  p.c = c;
+  p.ldc = ldc;
+  p.M = (int)a.rows;
+  p.N = (int)b.rows;
+  p.K = (int)a.cols;
+  const int macro = (a.mant ? a.macro_size : b.macro_size);
+  p.macro_steps = macro / KSTEP;
+  p.n_chunks = (int)((a.cols + macro - 1) / macro);
+  p.idesc = make_idesc(BN, ue8m0);
+  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
+  int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, NUM_THREADS, C::SMEM, st>>>(ta, tb, p);
+  return check_launch();
+}
+
+}  // namespace tc
+
 int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, uint32_t* status,
                    cudaStream_t st) {
-  (void)a; (void)b; (void)c; (void)c_dtype; (void)ldc; (void)status; (void)st;
-  return set_error(ERR_UNSUPPORTED, "tcgen05 GEMM not built yet");
+  (void)status;
+  using namespace tc;
+  if (!a.scales_mma || !b.scales_mma) return set_error(ERR_INVALID, "operands need the tcgen05 scale layout");
+  const bool nva = a.variant == NVFP4, nvb = b.variant == NVFP4;
+  if (nva != nvb) return set_error(ERR_UNSUPPORTED, "UE8M0 x UE4M3 operand pair has no block-scaled MMA form");
+  const bool mbs = (a.variant == MBS_S || a.variant == MBS_D || b.variant == MBS_S || b.variant == MBS_D);
+  const bool sf32 = (a.block_size == 32 && b.block_size == 32) && a.sf_kpad * 32 == b.sf_kpad * 32;
+  if (a.rows > (1 << 30) || b.rows > (1 << 30) || a.cols > (1 << 30)) return set_error(ERR_UNSUPPORTED, "shape too large");
+  if (mbs) {
+    const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
+    if ((ma && !a.mant_t) || (mb && !b.mant_t)) return set_error(ERR_INVALID, "MBS operand needs transposed mantissas");
+    const int macro = ma ? a.macro_size : b.macro_size;
+    if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
+    if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
+    if (c_dtype == MXQ_BF16) return launch_variant<128, 6, 3, false, true, true>(a, b, c, ldc, true, st);
+    return launch_variant<128, 6, 3, false, true, false>(a, b, c, ldc, true, st);
+  }
+  if (sf32) {
+    if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, true, false, true>(a, b, c, ldc, true, st);
+    return launch_variant<256, 4, 1, true, false, false>(a, b, c, ldc, true, st);
+  }
+  const bool ue8m0 = !nva;
+  if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, false, false, true>(a, b, c, ldc, ue8m0, st);
+  return launch_variant<256, 4, 1, false, false, false>(a, b, c, ldc, ue8m0, st);
 }
+
 }  // namespace mxq

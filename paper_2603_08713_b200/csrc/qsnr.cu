@@ -50,9 +50,9 @@ __device__ Range node_at(int64_t n, int depth, int64_t idx) {
   return {s, len};
 }
 
-// Enumerate the leaves of a node in left-to-right order (thread 0).
-__device__ int enum_leaves(Range r, Range* out) {
-  Range stack[64];
+// Enumerate the leaves of a node in left-to-right order (thread 0; the
+// explicit stack lives in shared memory -- no device recursion).
+__device__ int enum_leaves(Range r, Range* out, Range* stack) {
   int sp = 0, nl = 0;
   if (r.n > 0) stack[sp++] = r;
   while (sp) {
@@ -70,14 +70,41 @@ __device__ int enum_leaves(Range r, Range* out) {
 }
 
 struct PairSum { double a, b; };
+struct Frame { int64_t n; int state; double la, lb; };
 
-__device__ PairSum fold_node(int64_t len, int& k, const double* la, const double* lb) {
-  if (len == 0) return {0.0, 0.0};
-  if (len <= 128) { PairSum p{la[k], lb[k]}; ++k; return p; }
-  const int64_t n2 = pw_split(len);
-  PairSum x = fold_node(n2, k, la, lb);
-  PairSum y = fold_node(len - n2, k, la, lb);
-  return {__dadd_rn(x.a, y.a), __dadd_rn(x.b, y.b)};
+// Post-order fold of a node's subtree over its leaf sums (consumed in
+// left-to-right order): sum(node) = sum(left) + sum(right), exactly numpy's
+// recursion, evaluated iteratively with a shared-memory frame stack.
+__device__ PairSum fold_node(int64_t len, const double* la, const double* lb, Frame* st) {
+  int sp = 0, k = 0;
+  PairSum res{0.0, 0.0};
+  st[sp++] = {len, 0, 0.0, 0.0};
+  while (sp) {
+    Frame& f = st[sp - 1];
+    bool done = false;
+    if (f.n == 0) {
+      res = {0.0, 0.0};
+      done = true;
+    } else if (f.n <= 128) {
+      res = {la[k], lb[k]};
+      ++k;
+      done = true;
+    } else if (f.state == 0) {
+      f.state = 1;
+      st[sp++] = {pw_split(f.n), 0, 0.0, 0.0};
+    } else if (f.state == 1) {
+      f.la = res.a;
+      f.lb = res.b;
+      f.state = 2;
+      const int64_t n2 = pw_split(f.n);
+      st[sp++] = {f.n - n2, 0, 0.0, 0.0};
+    } else {
+      res = {__dadd_rn(f.la, res.a), __dadd_rn(f.lb, res.b)};
+      done = true;
+    }
+    if (done) --sp;
+  }
+  return res;
 }
 
 __device__ __forceinline__ float load_ref(const void* ref, int dtype, int64_t off) {
@@ -95,11 +122,13 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   __shared__ double s_sq[QS_WARPS][2][128];
   __shared__ int s_nl;
   __shared__ unsigned long long s_cnt[2];
+  __shared__ Range s_stack[64];
+  __shared__ Frame s_frames[64];
   const int64_t n = rows * cols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Range node = node_at(n, depth, blockIdx.x);
   if (threadIdx.x == 0) {
-    s_nl = enum_leaves(node, s_leaf);
+    s_nl = enum_leaves(node, s_leaf, s_stack);
     s_cnt[0] = s_cnt[1] = 0ull;
   }
   __syncthreads();
@@ -168,8 +197,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int k = 0;
-    PairSum ps = fold_node(node.n, k, s_la, s_lb);
+    PairSum ps = fold_node(node.n, s_la, s_lb, s_frames);
     const int64_t nodes = (int64_t)1 << depth;
     ws[blockIdx.x] = ps.a;
     ws[nodes + blockIdx.x] = ps.b;
@@ -179,24 +207,30 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   }
 }
 
-__device__ PairSum fold_top(int64_t len, int level, int depth, int64_t idx, const double* ws, int64_t nodes) {
-  if (level == depth) return {ws[idx], ws[nodes + idx]};
-  int64_t ln, rn;
-  if (len <= 128) { ln = len; rn = 0; }
-  else { ln = pw_split(len); rn = len - ln; }
-  PairSum x = fold_top(ln, level + 1, depth, 2 * idx, ws, nodes);
-  PairSum y = fold_top(rn, level + 1, depth, 2 * idx + 1, ws, nodes);
-  return {__dadd_rn(x.a, y.a), __dadd_rn(x.b, y.b)};
-}
-
-__global__ void k_qsnr_top(int64_t n, int depth, const double* __restrict__ ws, double* __restrict__ out4) {
+// Fold of the top `depth` levels.  Every CTA node sits at depth d of a
+// perfect binary tree (a numpy leaf above depth d continues as "left = itself,
+// right = empty (0.0)"), so the top of the tree is a plain pairwise
+// reduction of the 2^d node sums in index order -- done in place.
+__global__ void k_qsnr_top(int64_t n, int depth, double* __restrict__ ws, double* __restrict__ out4) {
   const int64_t nodes = (int64_t)1 << depth;
-  PairSum ps = fold_top(n, 0, depth, 0, ws, nodes);
-  const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(ws + 2 * nodes);
-  out4[0] = ps.a;
-  out4[1] = ps.b;
-  out4[2] = (double)cnt[0];
-  out4[3] = (double)cnt[1];
+  double* sa = ws;
+  double* sb = ws + nodes;
+  for (int64_t width = nodes; width > 1; width >>= 1) {
+    // single thread, ascending i: slot i is written only after slots 2i and
+    // 2i+1 (>= i) have been read
+    for (int64_t i = 0; i < width / 2; ++i) {
+      sa[i] = __dadd_rn(sa[2 * i], sa[2 * i + 1]);
+      sb[i] = __dadd_rn(sb[2 * i], sb[2 * i + 1]);
+    }
+  }
+  {
+    const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(ws + 2 * nodes);
+    out4[0] = sa[0];
+    out4[1] = sb[0];
+    out4[2] = (double)cnt[0];
+    out4[3] = (double)cnt[1];
+  }
+  (void)n;
 }
 
 int64_t qsnr_workspace_bytes(int64_t n) {
@@ -216,7 +250,6 @@ int launch_qsnr(const void* ref, int dtype, int64_t ref_ld, const QDesc* q, cons
   if (q) qd = *q;
   k_qsnr_nodes<<<(unsigned)nodes, QS_THREADS, 0, st>>>(ref, dtype, ref_ld, qd, q ? 1 : 0, recon, recon_ld, rows,
                                                          cols, d, w, status);
-  // the top fold recurses on one thread: give it a deep enough stack
   k_qsnr_top<<<1, 1, 0, st>>>(n, d, w, out4);
   return check_launch();
 }

@@ -214,14 +214,12 @@ __global__ void __launch_bounds__(256) k_quantize_mbs_s(const void* __restrict__
 constexpr int MBSD_THREADS = 128;
 constexpr int MBSD_STRIDE = 17;  // doubles per lane slot (16 + 1 pad)
 
-__device__ double pw_sum_smem(const double* lane_base, int64_t start, int64_t n);
-
 // Element p of a macro lives in lane p/16, slot p%16.
 __device__ __forceinline__ double sq_at(const double* base, int64_t p) {
   return base[(p >> 4) * MBSD_STRIDE + (p & 15)];
 }
 
-__device__ double pw_leaf_smem(const double* base, int64_t s, int64_t n) {
+__device__ __forceinline__ double pw_leaf_smem(const double* base, int64_t s, int64_t n) {
   if (n < 8) {
     double acc = 0.0;
     for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, sq_at(base, s + i));
@@ -241,11 +239,20 @@ __device__ double pw_leaf_smem(const double* base, int64_t s, int64_t n) {
   return res;
 }
 
-__device__ double pw_sum_smem(const double* base, int64_t s, int64_t n) {
-  if (n <= 128) return pw_leaf_smem(base, s, n);
-  int64_t n2 = pw_split(n);
-  return __dadd_rn(pw_sum_smem(base, s, n2), pw_sum_smem(base, s + n2, n - n2));
+// numpy's split recursion, unrolled at compile time (no device recursion):
+// macro widths <= 512 need at most 2 split levels, D = 3 covers <= 1024.
+template <int D>
+__device__ __forceinline__ double pw_sum_smem_t(const double* base, int64_t s, int64_t n) {
+  if constexpr (D == 0) {
+    return pw_leaf_smem(base, s, n);
+  } else {
+    if (n <= 128) return pw_leaf_smem(base, s, n);
+    const int64_t n2 = pw_split(n);
+    return __dadd_rn(pw_sum_smem_t<D - 1>(base, s, n2), pw_sum_smem_t<D - 1>(base, s + n2, n - n2));
+  }
 }
+
+__device__ double pw_sum_smem(const double* base, int64_t s, int64_t n) { return pw_sum_smem_t<3>(base, s, n); }
 
 __constant__ uint8_t c_cands[256];
 // LUT mode table (src/quantize.py:482-504): [regime][candidate][bin] fp16

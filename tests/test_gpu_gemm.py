@@ -1,0 +1,92 @@
+"""GPU parity of the tcgen05 block-scaled GEMM against the reference
+dequantise-then-f64-matmul.
+
+Tolerance: relative Frobenius error <= 1e-5 AND
+per element |dC_ij| <= 2^-16 * (|A| |B|^T)_ij, where A, B are the
+reference-dequantised operands.  The tensor core accumulates FP4 products in
+f32 (and the MBS sigma is applied per 128-K chunk in f32), so bit-exactness
+is not expected; any scale-index / sigma / layout bug shows up as O(1e-2).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import mxq_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_2603_08713_b200 as M  # noqa: E402
+
+PAIRS = [("mx16", "mx16"), ("mx16_oas", "mx16_oas"), ("ocp32", "ocp32"), ("mbs_s", "mbs_d"),
+         ("mbs_s", "mx16_oas"), ("mx16_oas", "mbs_d"), ("ocp32", "mx16"), ("nvfp4", "nvfp4"), ("mbs_d", "mbs_d")]
+SHAPES = [(128, 256, 256), (256, 512, 1024), (200, 300, 2880), (33, 29, 384), (1, 128, 4096), (384, 256, 512)]
+
+
+def _ref(a, b, va, vb):
+    qa, qb = O.quantize(a, va), O.quantize(b, vb)
+    da, db = O.dequantize(qa).astype(np.float64), O.dequantize(qb).astype(np.float64)
+    return da @ db.T, np.abs(da) @ np.abs(db).T
+
+
+def _check(c, want, bound, tag):
+    c = c.astype(np.float64)
+    rel = np.linalg.norm(c - want) / max(np.linalg.norm(want), 1e-300)
+    assert rel <= 1e-5, (tag, rel)
+    excess = np.abs(c - want) - 2.0 ** -16 * bound
+    assert np.all(excess <= 0), (tag, float(excess.max()), np.unravel_index(np.argmax(excess), excess.shape))
+
+
+@pytest.mark.parametrize("va,vb", PAIRS)
+def test_tc_gemm_matches_reference(va, vb):
+    rng = np.random.Generator(np.random.PCG64(103))
+    for (m, n, k) in SHAPES:
+        if (va == "ocp32" or vb == "ocp32") and k % 32:
+            continue
+        a = rng.standard_t(4, (m, k)).astype(np.float32)
+        b = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+        aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant(va)))
+        bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant(vb)))
+        assert M.tc_supported(aq, bq)
+        c = M.matmul_quantized(aq, bq).cpu().numpy()
+        want, bound = _ref(a, b, va, vb)
+        _check(c, want, bound, (va, vb, m, n, k))
+        c2 = M.matmul_quantized(aq, bq).cpu().numpy()
+        assert np.array_equal(c, c2), "non-deterministic"
+        cb = M.matmul_quantized(aq, bq, out_dtype=torch.bfloat16).float().cpu().numpy()
+        assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
+
+
+def test_tc_gemm_llama_shape_mbs_h():
+    """One Llama-3-8B O-proj sized MBS-H product (A MBS_S x W MBS_D)."""
+    rng = np.random.Generator(np.random.PCG64(5))
+    a = rng.standard_t(4, (512, 4096)).astype(np.float32)
+    w = (rng.standard_normal((1024, 4096)) * 0.02).astype(np.float32)
+    aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S))
+    wq = M.quantize_tensor(w, M.SchemeConfig(M.Variant.MBS_D))
+    c = M.matmul_quantized(aq, wq).cpu().numpy()
+    want, bound = _ref(a, w, "mbs_s", "mbs_d")
+    _check(c, want, bound, "llama")
+
+
+def test_mixed_scale_types_route_to_exact():
+    rng = np.random.Generator(np.random.PCG64(9))
+    a = rng.standard_normal((40, 256)).astype(np.float32)
+    b = rng.standard_normal((24, 256)).astype(np.float32)
+    aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_D))
+    bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant.NVFP4))
+    assert not M.tc_supported(aq, bq)
+    c = M.matmul_quantized(aq, bq).cpu().numpy()
+    assert np.array_equal(c, O.matmul_quantized(O.quantize(a, "mbs_d"), O.quantize(b, "nvfp4")))
+
+
+def test_tk_validation_like_reference():
+    rng = np.random.Generator(np.random.PCG64(106))
+    a = rng.standard_normal((8, 256)).astype(np.float32)
+    q16 = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MX16))
+    qm = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_D))
+    with pytest.raises(ValueError):
+        M.matmul_quantized(q16, q16, M.TileConfig(8, 8, 24))
+    with pytest.raises(ValueError):
+        M.matmul_quantized(qm, qm, M.TileConfig(8, 8, 64))
+    M.matmul_quantized(qm, qm, M.TileConfig(8, 8, 256))
