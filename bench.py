@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MXFP4 quantize-and-GEMM path (BASELINE.json configs[1]).
+
+Workload (one "step"): the four Llama-3-8B linear layers at M = 4096 tokens --
+QKV (N 6144, K 4096), O (4096, 4096), gate_up (28672, 4096), down (4096, 14336)
+-- each = quantize the bf16 activation on the fly (MBS-S) and run the tcgen05
+block-scaled GEMM against resident MBS-D weights (MBS-H, the paper's default),
+bf16 output.  Synthetic data: activations gaussian with 1% x100 outliers,
+random-init weights N(0, 0.02).  Headline `value` = step TFLOP/s (device-timed,
+inputs resident in HBM); `e2e` = the same step through the public API with
+pinned host activations in and bf16 products out.  Comparison arms on the
+same shapes: plain MXFP4 (OCP32 block-32, kind::mxf4), MX16+OAS and NVFP4.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): every layer is column-sharded (weight rows) across ranks and
+the bf16 outputs are all-gathered over NVLink (strong scaling, SURVEY §8 e).
+`--impl reference` times the reference algorithm (the CPU oracle port,
+oracle/mxq_oracle.py) on the host cores on a bounded row sample of the same
+workload; under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "OAS+MBS MXFP4 GEMM TFLOPS & overhead vs plain MXFP4/NVFP4; quant GB/s; QSNR"
+LAYERS = (("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336))
+M_TOK = 4096
+WORKLOAD = ("llama3-8b linear layers QKV 6144x4096, O 4096x4096, gate_up 28672x4096, down 4096x14336; "
+            "M=4096 tokens; A quantized per step (MBS_S) x resident W (MBS_D) = MBS-H; bf16 out")
+
+
+def flops_per_step(m=M_TOK, n_scale=1.0):
+    return sum(2.0 * m * n * k for _, n, k in LAYERS) * n_scale
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_08713_b200 as M
+    from paper_2603_08713_b200 import parallel as P
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    V = M.Variant
+    bf16 = torch.bfloat16
+
+    # ---- synthetic inputs (activations replicated, weights sharded) --------
+    g = torch.Generator(device=dev).manual_seed(1234)
+    acts = []
+    for _, n, k in LAYERS:
+        x = torch.randn(M_TOK, k, device=dev, generator=g)
+        hit = torch.rand(M_TOK, k, device=dev, generator=g) < 0.01
+        acts.append(torch.where(hit, x * 100.0, x).to(bf16))
+    gw = torch.Generator(device=dev).manual_seed(4321 + rank)
+    wdense, bounds = [], []
+    for _, n, k in LAYERS:
+        lo, hi = P.shard_bounds(n, world, rank)
+        bounds.append((lo, hi))
+        wdense.append((torch.randn(hi - lo, k, device=dev, generator=gw) * 0.02).to(bf16))
+
+    arms = {  # name -> (activation variant, weight variant)
+        "mbs_h": (V.MBS_S, V.MBS_D),
+        "ocp32": (V.OCP32, V.OCP32),
+        "mx16_oas": (V.MX16_OAS, V.MX16_OAS),
+        "nvfp4": (V.NVFP4, V.NVFP4),
+    }
+    weights = {name: [M.quantize_tensor(w, M.SchemeConfig(wv)) for w in wdense] for name, (_, wv) in arms.items()}
+    del wdense
+    outs = [torch.empty(M_TOK, hi - lo, device=dev, dtype=bf16) for lo, hi in bounds]
+    gathered = [torch.empty(world * M_TOK, max(P.shard_bounds(n, world, r)[1] - P.shard_bounds(n, world, r)[0]
+                                               for r in range(world)), device=dev, dtype=bf16)
+                if world > 1 else None for _, n, _ in LAYERS]
+    n_local_frac = sum(2.0 * M_TOK * (hi - lo) * k for (lo, hi), (_, _, k) in zip(bounds, LAYERS))
+    step_flops_global = flops_per_step()
+
+    def step(arm, gemm_events=None):
+        av, _ = arms[arm]
+        for li in range(len(LAYERS)):
+            aq = M.quantize_tensor(acts[li], M.SchemeConfig(av), check=False)
+            if gemm_events is not None:
+                gemm_events[li][0].record()
+            M.matmul_quantized(aq, weights[arm][li], out=outs[li], out_dtype=bf16, check=False)
+            if gemm_events is not None:
+                gemm_events[li][1].record()
+            if world > 1:
+                send = outs[li]
+                if send.shape[1] != gathered[li].shape[1]:
+                    pad = torch.zeros(M_TOK, gathered[li].shape[1], device=dev, dtype=bf16)
+                    pad[:, : send.shape[1]] = send
+                    send = pad
+                dist.all_gather_into_tensor(gathered[li], send)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def time_steps(arm, k, w):
+        for _ in range(w):
+            step(arm)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            step(arm)
+        e1.record()
+        barrier()
+        ms = e0.elapsed_time(e1) / k
+        return P.max_over_ranks(ms, device=dev)
+
+    def time_gemms(arm, k):
+        """Per-launch device time of the dominant kernel (the GEMM)."""
+        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in LAYERS] for _ in range(k)]
+        barrier()
+        for i in range(k):
+            step(arm, evs[i])
+        barrier()
+        per_layer = [float(np.mean([evs[i][li][0].elapsed_time(evs[i][li][1]) for i in range(k)]))
+                     for li in range(len(LAYERS))]
+        return per_layer
+
+    K, W = args.steps, args.warmup
+    results = {}
+    with Clocks(local) as clocks:
+        for arm in ("mbs_h", "ocp32", "mx16_oas", "nvfp4"):
+            ms = time_steps(arm, K, W)
+            gl = time_gemms(arm, max(3, K // 2))
+            gemm_ms = sum(gl)
+            results[arm] = {
+                "ms_per_step": ms,
+                "tflops_step": step_flops_global / (ms * 1e-3) / 1e12,
+                "gemm_ms": gemm_ms,
+                "gemm_tflops": n_local_frac / (gemm_ms * 1e-3) / 1e12 * world,
+                "gemm_ms_per_layer": {name: t for (name, _, _), t in zip(LAYERS, gl)},
+            }
+    head = results["mbs_h"]
+
+    # ---- quantizer bandwidth (4096x4096 bf16 activation, one launch) -------
+    qbw = {}
+    x = acts[0]
+    bytes_per_el = {"ocp32": 2 + 0.5 + 1 / 32, "mx16": 2 + 0.5 + 1 / 16, "mx16_oas": 2 + 0.5 + 1 / 16,
+                    "mbs_s": 2 + 0.5 + 1 / 16 + 1 / 128, "mbs_d": 2 + 0.5 + 1 / 16 + 1 / 128,
+                    "nvfp4": 2 + 0.5 + 1 / 16}
+    for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "nvfp4", "mbs_d"):
+        cfg = M.SchemeConfig(V(vname))
+        reps = 5 if vname == "mbs_d" else 20
+        for _ in range(3):
+            M.quantize_tensor(x, cfg, check=False, gemm_layout=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            M.quantize_tensor(x, cfg, check=False, gemm_layout=False)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        qbw[vname] = {"us": ms * 1e3, "gbs": x.numel() * bytes_per_el[vname] / (ms * 1e-3) / 1e9,
+                      "melem_s": x.numel() / (ms * 1e-3) / 1e6}
+
+    out = None
+    if rank == 0:
+        out = {}
+        # ---- QSNR on config 1 (4096x4096 gaussian+outliers seed 0, bf16) ----
+        t1 = M.generate_tensor(M.GeneratorSpec("gaussian_with_outliers", (4096, 4096), seed=0))
+        t1b = torch.from_numpy(t1).to(dev).to(bf16)
+        meta = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_meta.json")))
+        qs = {}
+        for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4"):
+            q = M.quantize_tensor(t1b, M.SchemeConfig(V(vname)))
+            rep, fl = M.qsnr_quantized(t1b, q)
+            ref = meta["config1"][vname]
+            qs[vname] = {"qsnr_db": round(rep.qsnr_db, 6), "flush": round(fl, 6),
+                         "equals_reference": rep.qsnr_db == ref["qsnr_db"] and fl == ref["flush"]}
+        out["qsnr"] = qs
+
+        # ---- e2e: public API, pinned host activations in, bf16 out ---------
+        if world == 1:
+            host_in = [a.cpu().pin_memory() for a in acts]
+            host_out = [torch.empty(o.shape, dtype=bf16).pin_memory() for o in outs]
+            cfg_a = M.SchemeConfig(V.MBS_S)
+
+            def e2e_step():
+                for li in range(len(LAYERS)):
+                    aq = M.quantize_tensor(host_in[li], cfg_a)      # H2D + quantize (+ status check)
+                    c = M.matmul_quantized(aq, weights["mbs_h"][li], out_dtype=bf16)
+                    host_out[li].copy_(c, non_blocking=True)        # D2H of the product
+                torch.cuda.synchronize()
+
+            for _ in range(max(2, W // 2)):
+                e2e_step()
+            ke = max(3, K // 2)
+            t0 = time.perf_counter()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(ke):
+                e2e_step()
+            e1.record()
+            torch.cuda.synchronize()
+            ms_e2e = e0.elapsed_time(e1) / ke
+            out["e2e"] = {"value": step_flops_global / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+                          "h2d_bytes_per_step": int(sum(a.numel() * 2 for a in acts)),
+                          "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)),
+                          "ms_per_step": ms_e2e, "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / ke}
+        else:
+            out["e2e"] = None
+    if world > 1:
+        dist.barrier(device_ids=[local])
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (tcgen05 GEMM, MBS-H) -------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16_peak = peaks.get("bf16_tflops")
+    basis = "4 x measured dense bf16 (MEASURED_PEAKS.json bf16_tflops, burst): FP4 dense = 4x bf16 on B200"
+    if not bf16_peak:
+        bf16_peak, basis = 1590.0, "4 x fallback dense bf16 1.59 PF (B200_PROFILING.md)"
+    fp4_peak = 4.0 * bf16_peak
+    achieved = head["gemm_tflops"]
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("mbs_h_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(fp4_peak, 1), "unit": "TFLOP/s",
+                "frac": round(achieved / fp4_peak, 4), "traffic": traffic, "peak_basis": basis,
+                "kernel": "k_gemm_tc<128,5,3,mxf4nvf4 UE8M0,MBS,bf16>",
+                "algorithmic": "2*M*N*K per launch over the 4 layer launches, CUDA events on the launch stream"}
+
+    # ---- CPU baseline: the reference algorithm (oracle port) on a sample ---
+    cpu = cpu_baseline_sample(weights_from_gpu=[weights["mbs_h"][li] for li in range(len(LAYERS))],
+                              acts=acts, rows=args.cpu_rows)
+
+    ocp = results["ocp32"]
+    line = {
+        "metric": METRIC, "value": round(head["tflops_step"], 2), "unit": "TFLOP/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
+        "data": "synthetic (activations N(0,1) with 1% x100 outliers; random-init N(0,0.02) weights)",
+        "config": {"workload": WORKLOAD, "global_batch": M_TOK, "seq_len": None,
+                   "parallelism": f"column-shard x{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (218 MB bf16 activations + 121 MB fp4 weights per step)"},
+        "gemm_only_tflops": round(head["gemm_tflops"], 2),
+        "arms": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                 for k, v in results.items()},
+        "mbs_h_overhead_vs_ocp32": round(1.0 - head["tflops_step"] / ocp["tflops_step"], 4),
+        "mbs_h_gemm_overhead_vs_ocp32": round(1.0 - head["gemm_tflops"] / ocp["gemm_tflops"], 4),
+        "mbs_h_overhead_vs_nvfp4": round(1.0 - head["tflops_step"] / results["nvfp4"]["tflops_step"], 4),
+        "quantizer": {k: {kk: round(vv, 2) for kk, vv in v.items()} for k, v in qbw.items()},
+        "quantizer_hbm_frac_mbs_s": round(qbw["mbs_s"]["gbs"] / peaks.get("hbm_gbs", 6650.0), 4),
+        "qsnr_config1": out["qsnr"],
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": out["e2e"],
+        "gpu_launches": 8 * K,
+        "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline_sample(weights_from_gpu, acts, rows: int):
+    """Reference algorithm on the host cores: quantize a row sample of every
+    layer's activation with the CPU oracle (MBS-S), dequantize, f64 GEMM
+    against the dequantized MBS-D weights (weights prepared outside the
+    timed region, as on the GPU)."""
+    import torch
+
+    from oracle import mxq_oracle as O
+
+    wdq = []
+    for q in weights_from_gpu:
+        h = q.to_host()
+        oq = O.OracleQ("mbs_d", h["shape"], 16, 128, h["codes"], h["block_scales"], None, h["mbs_mantissas"], None)
+        wdq.append(O.dequantize(oq).astype(np.float64))
+    samples = [a[:rows].float().cpu().numpy() for a in acts]
+    t0 = time.perf_counter()
+    flops = 0.0
+    for x, w in zip(samples, wdq):
+        q = O.quantize(x, "mbs_s")
+        xd = O.dequantize(q).astype(np.float64)
+        c = (xd @ w.T).astype(np.float32)
+        flops += 2.0 * x.shape[0] * w.shape[0] * w.shape[1]
+    dt = time.perf_counter() - t0
+    return {"value": round(flops / dt / 1e12, 6), "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{rows} of 4096 token rows per layer, all 4 layers (MBS_S quantize + dequant + f64 BLAS "
+                      f"GEMM vs pre-dequantized MBS_D weights); {dt:.2f} s"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference algorithm (oracle port) on the host cores
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    from concurrent.futures import ProcessPoolExecutor
+
+    from oracle import mxq_oracle as O
+
+    cores = os.cpu_count() or 1
+    rows = args.ref_rows
+    rng = np.random.Generator(np.random.PCG64(1234))
+    wrng = np.random.Generator(np.random.PCG64(4321))
+    # weights: MBS-D on a column sample (prepared outside the timed region)
+    ncols_sample = args.ref_wrows
+    with ProcessPoolExecutor(max_workers=cores) as pool:
+        wdq = []
+        for _, n, k in LAYERS:
+            w = (wrng.standard_normal((min(n, ncols_sample), k)) * 0.02).astype(np.float32)
+            wdq.append(O.dequantize(O.quantize_sharded(w, "mbs_d", cores, pool)).astype(np.float64))
+        acts = []
+        for _, n, k in LAYERS:
+            x = rng.standard_normal((rows, k))
+            x = np.where(rng.random((rows, k)) < 0.01, x * 100, x).astype(np.float32)
+            acts.append(O.bf16_round(x))
+
+        def step():
+            fl = 0.0
+            for x, w in zip(acts, wdq):
+                q = O.quantize_sharded(x, "mbs_s", cores, pool)
+                xd = O.dequantize(q).astype(np.float64)
+                _ = (xd @ w.T).astype(np.float32)
+                fl += 2.0 * x.shape[0] * w.shape[0] * w.shape[1]
+            return fl
+
+        for _ in range(args.warmup):
+            step()
+        t0 = time.perf_counter()
+        fl = 0.0
+        for _ in range(args.steps):
+            fl += step()
+        dt = (time.perf_counter() - t0) / args.steps
+    val = fl / args.steps / dt / 1e12
+    line = {
+        "metric": METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": env_int("WORLD_SIZE", 1),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp64 reference arithmetic (numpy)",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOAD, "global_batch": M_TOK, "seq_len": None, "parallelism": "host cores"},
+        "cpu_baseline": {"value": round(val, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                         "sample": f"{rows} token rows x {ncols_sample} weight rows per layer (4 layers): "
+                                   f"row-sharded MBS_S quantize over {cores} processes + dequant + f64 BLAS GEMM"},
+        "e2e": {"value": round(val, 6), "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cpu-rows", type=int, default=256)
+    ap.add_argument("--ref-rows", type=int, default=256)
+    ap.add_argument("--ref-wrows", type=int, default=2048)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -68,9 +68,10 @@ extern "C" {
  * GEMM-side copies (either may be NULL when not needed):
  *  - scales_mma: the tcgen05 scale-factor atom layout, 512-byte atoms of
  *    128 rows x 4 blocks ordered [row/128][block/4], byte
- *    (r%32)*16 + ((r%128)/32)*4 + block%4.  Rows padded to a multiple of 128,
+ *    (r%32)*16 + ((r%128)/32)*4 + block%4.  Rows padded to a multiple of 256,
  *    blocks per row padded to `sf_kpad` (a multiple of 256/block_size).
- *  - mant_t: mantissa bytes transposed to (n_macros, mant_t_ld >= rows).
+ *  - sig_t: the MBS factor sigma = 1/(1+m8/256) as f32, transposed to
+ *    (n_macros, sig_t_ld >= rows) so a GEMM chunk reads it contiguously.
  */
 typedef struct mxq_qtensor {
   int32_t variant;     /* MXQ_OCP32 .. MXQ_NVFP4 */
@@ -82,7 +83,7 @@ typedef struct mxq_qtensor {
   uint8_t* scales;      int64_t scales_ld;  /* bytes between rows, >= cols/bs  */
   uint8_t* scales_mma;  int64_t sf_kpad;    /* padded blocks per row            */
   uint8_t* mant;        int64_t mant_ld;    /* (rows, n_macros) mantissa bytes  */
-  uint8_t* mant_t;      int64_t mant_t_ld;  /* (n_macros, rows) transposed copy */
+  float* sig_t;         int64_t sig_t_ld;   /* (n_macros, rows) sigma = 1/(1+m8/256), f32 */
   double* tensor_scale;                     /* NVFP4 s_t (device f64)           */
 } mxq_qtensor;
 
@@ -138,7 +139,7 @@ int mxq_qsnr(const void* ref, int32_t ref_dtype, int64_t ref_ld, const mxq_qtens
 
 /*
  * Block-scaled tcgen05 GEMM  C[M,N] = A[M,K] . B[N,K]^T  on quantized
- * operands (K-major codes, scales_mma, and for MBS operands mant_t).
+ * operands (K-major codes, scales_mma, and for MBS operands sig_t).
  * Replaces: matmul_quantized src/gemm.py:137-172 (tolerance parity: the MMA
  * accumulates FP4 products in f32 per 64-K step; the MBS factor
  * sigma = 1/(1+m8/256) of each operand is applied per 128-K macro chunk
@@ -167,7 +168,7 @@ int mxq_gemm_exact(const mxq_qtensor* a, const mxq_qtensor* b, float* c, int64_t
 int mxq_matmul_reference(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t m, int64_t n, int64_t k,
                          float* c, int64_t ldc, void* stream);
 
-/* Build the GEMM-side copies (scales_mma, mant_t) from the row-major fields
+/* Build the GEMM-side copies (scales_mma, sig_t) from the row-major fields
  * of a user-constructed QuantizedTensor. */
 int mxq_build_gemm_layout(const mxq_qtensor* q, int32_t sf_block, void* stream);
 

@@ -35,7 +35,7 @@ class QT(ctypes.Structure):
         ("scales", ctypes.c_void_p), ("scales_ld", ctypes.c_int64),
         ("scales_mma", ctypes.c_void_p), ("sf_kpad", ctypes.c_int64),
         ("mant", ctypes.c_void_p), ("mant_ld", ctypes.c_int64),
-        ("mant_t", ctypes.c_void_p), ("mant_t_ld", ctypes.c_int64),
+        ("sig_t", ctypes.c_void_p), ("sig_t_ld", ctypes.c_int64),
         ("tensor_scale", ctypes.c_void_p),
     ]
 

@@ -99,17 +99,17 @@ int mxq_quantize(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor
   if (((uintptr_t)x % 16) || ((x_ld * esz) % 16)) return set_error(ERR_UNSUPPORTED, "input must be 16-byte aligned with a 16-byte row pitch");
   if (!q->scales && !q->scales_mma) return set_error(ERR_INVALID, "no scale output buffer");
   const bool mbs = q->variant == MBS_S || q->variant == MBS_D;
-  if (mbs && !q->mant && !q->mant_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
+  if (mbs && !q->mant && !q->sig_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
   if (q->scales_mma) {  // padding atoms must hold finite scale codes
-    const int64_t rows_pad = (q->rows + 127) / 128 * 128;
+    const int64_t rows_pad = (q->rows + 255) / 256 * 256;
     if (rows_pad != q->rows || q->sf_kpad != q->cols / q->block_size) {
       cudaError_t e = cudaMemsetAsync(q->scales_mma, 0, (size_t)(rows_pad * q->sf_kpad), (cudaStream_t)stream);
       if (e != cudaSuccess) return set_cuda_error(e);
     }
   }
-  if (q->mant_t && q->mant_t_ld > q->rows) {
+  if (q->sig_t && q->sig_t_ld > q->rows) {
     const int64_t nmac = (q->cols + q->macro_size - 1) / q->macro_size;
-    cudaError_t e = cudaMemsetAsync(q->mant_t, 0, (size_t)(nmac * q->mant_t_ld), (cudaStream_t)stream);
+    cudaError_t e = cudaMemsetAsync(q->sig_t, 0, sizeof(float) * (size_t)(nmac * q->sig_t_ld), (cudaStream_t)stream);
     if (e != cudaSuccess) return set_cuda_error(e);
   }
   return launch_quantize(x, x_dtype, x_ld, *q, mbs_mode, cand, n_cand, augment_static, scratch,
@@ -125,9 +125,9 @@ int mxq_quantize_mbs_lut(const void* x, int32_t x_dtype, int64_t x_ld, const mxq
   const int esz = x_dtype == DT_BF16 ? 2 : 4;
   if (x_ld < q->cols || ((uintptr_t)x % 16) || ((x_ld * esz) % 16))
     return set_error(ERR_UNSUPPORTED, "input must be 16-byte aligned with a 16-byte row pitch");
-  if (!q->mant && !q->mant_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
+  if (!q->mant && !q->sig_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
   if (q->scales_mma) {
-    const int64_t rows_pad = (q->rows + 127) / 128 * 128;
+    const int64_t rows_pad = (q->rows + 255) / 256 * 256;
     if (rows_pad != q->rows || q->sf_kpad != q->cols / q->block_size) {
       cudaError_t e = cudaMemsetAsync(q->scales_mma, 0, (size_t)(rows_pad * q->sf_kpad), (cudaStream_t)stream);
       if (e != cudaSuccess) return set_cuda_error(e);
@@ -199,7 +199,7 @@ int mxq_build_gemm_layout(const mxq_qtensor* q, int32_t sf_block, void* stream) 
   if (sf_block > q->block_size) return set_error(ERR_INVALID, "sf_block larger than block_size");
   if (q->scales_mma && (q->sf_kpad < q->cols / sf_block || q->sf_kpad % (256 / sf_block)))
     return set_error(ERR_INVALID, "sf_kpad must cover cols and be a multiple of 256/sf_block");
-  if (q->mant_t && q->mant_t_ld < q->rows) return set_error(ERR_INVALID, "mant_t_ld < rows");
+  if (q->sig_t && q->sig_t_ld < q->rows) return set_error(ERR_INVALID, "sig_t_ld < rows");
   return launch_build_gemm_layout(*q, sf_block, (cudaStream_t)stream);
 }
 

@@ -160,6 +160,23 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// acc{0,1} += (sa * sb{0,1}) * p{0,1} with packed f32x2 multiply / FMA
+// (FMUL2 + FFMA2): the MBS epilogue is bound by these two FP32 ops per output
+// per macro chunk.
+__device__ __forceinline__ void fma2_scaled(float& acc0, float& acc1, float sa, float sb0, float sb1, float p0,
+                                            float p1) {
+  asm("{\n\t.reg .b64 w, q, c, s;\n\t"
+      "mov.b64 w, {%2, %3};\n\t"
+      "mov.b64 s, {%6, %6};\n\t"
+      "mov.b64 q, {%4, %5};\n\t"
+      "mov.b64 c, {%0, %1};\n\t"
+      "mul.rn.f32x2 w, w, s;\n\t"
+      "fma.rn.f32x2 c, w, q, c;\n\t"
+      "mov.b64 {%0, %1}, c;\n\t}"
+      : "+f"(acc0), "+f"(acc1)
+      : "f"(sb0), "f"(sb1), "f"(p0), "f"(p1), "f"(sa));
+}
+
 __device__ __forceinline__ void epi_bar_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
 }
@@ -171,9 +188,9 @@ struct Params {
   const uint8_t* sfa;   // scale-factor atoms, [M/128][kgroups][512]
   const uint8_t* sfb;
   int64_t sfa_kg, sfb_kg;  // 4-block groups per 128-row block (sf_kpad / 4)
-  const uint8_t* mta;   // transposed mantissas (n_macros, ld) or null
-  const uint8_t* mtb;
-  int64_t mta_ld, mtb_ld;
+  const float* sga;     // MBS sigma, transposed (n_macros, ld) f32, or null (sigma = 1)
+  const float* sgb;
+  int64_t sga_ld, sgb_ld;
   const double* tsa;    // NVFP4 tensor scales or null
   const double* tsb;
   void* c;
@@ -194,9 +211,12 @@ struct Cfg {
   static constexpr int OFF_B = OFF_A + STAGES * STAGE_BYTES_A;
   static constexpr int OFF_SFA = OFF_B + STAGES * STAGE_BYTES_B;
   static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
-  static constexpr int OFF_SIGB = OFF_SFB + STAGES * SFB_BYTES;       // MBS: 2 x BN floats
-  static constexpr int OFF_BAR = OFF_SIGB + (MBS ? 2 * BN * 4 : 0);
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB;
+  // MBS sigma ring: NSIG slots of {sigmaA[BM], sigmaB[BN]} f32, one per chunk.
+  static constexpr int NSIG = MBS ? 8 : 0;
+  static constexpr int SIG_SLOT = (BM + BN) * 4;
+  static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
+  static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
   static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
   // TMEM columns: NB accumulators of BN columns, then 2 parity sets of SF.
@@ -219,7 +239,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + NB;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + NB);
+  uint64_t* sfull = tempty + NB;
+  uint64_t* sempty = sfull + C::NSIG;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sempty + C::NSIG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
@@ -235,6 +257,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], NUM_EPI_WARPS);
+    }
+    for (int b = 0; b < C::NSIG; ++b) {
+      mbar_init(&sfull[b], 1);
+      mbar_init(&sempty[b], NUM_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -338,6 +364,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (open) tc_commit(&tfull[buf]);
       }
     }
+  } else if (warp == 2) {
+    // ===================== sigma producer (MBS) =====================
+    if constexpr (MBS) {
+      if (lane == 0) {
+        const uint32_t bytes = (p.sga ? BM * 4 : 0) + (p.sgb ? BN * 4 : 0);
+        uint32_t ctr = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+          const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+          for (int t = 0; t < p.n_chunks; ++t, ++ctr) {
+            const uint32_t slot = ctr % C::NSIG;
+            mbar_wait(&sempty[slot], ((ctr / C::NSIG) & 1) ^ 1);
+            mbar_expect_tx(&sfull[slot], bytes);
+            float* dst = reinterpret_cast<float*>(smem + C::OFF_SIG + slot * C::SIG_SLOT);
+            if (p.sga) bulk_load(dst, p.sga + (int64_t)t * p.sga_ld + m0, BM * 4, &sfull[slot]);
+            if (p.sgb) bulk_load(dst + BM, p.sgb + (int64_t)t * p.sgb_ld + n0, BN * 4, &sfull[slot]);
+          }
+        }
+      }
+    }
   } else if (warp >= EPI_WARP0) {
     // ===================== epilogue =====================
     const int e = warp - EPI_WARP0;        // 0..7
@@ -373,19 +418,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else {
 #pragma unroll
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
-        float* sigb = reinterpret_cast<float*>(smem + C::OFF_SIGB);
-        const int et = threadIdx.x - EPI_WARP0 * 32;  // 0..255
         for (int t = 0; t < p.n_chunks; ++t) {
-          // sigma_B for this chunk's BN columns -> shared (parity buffer)
-          if (et < BN) {
-            float sb = 1.0f;
-            if (p.mtb) sb = 1.0f / mbs_factor(p.mtb[(int64_t)t * p.mtb_ld + n0 + et]);
-            sigb[(t & 1) * BN + et] = sb;
-          }
-          float sa = 1.0f;
-          if (p.mta) sa = 1.0f / mbs_factor(p.mta[(int64_t)t * p.mta_ld + m0 + row_in_tile]);
-          epi_bar_sync();
-          const float* sbp = sigb + (t & 1) * BN + half * COLS;
+          const uint32_t slot = chunk_ctr % C::NSIG;
+          mbar_wait(&sfull[slot], (chunk_ctr / C::NSIG) & 1);
+          const float* sig = reinterpret_cast<const float*>(smem + C::OFF_SIG + slot * C::SIG_SLOT);
+          const float sa = p.sga ? sig[row_in_tile] : 1.0f;
+          const float* sbp = sig + BM + half * COLS;
+          const bool hasb = p.sgb != nullptr;
           const uint32_t buf = chunk_ctr % NB;
           mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
           tc_fence_after();
@@ -395,11 +434,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             tmem_ld32(tmem + lane_addr + buf * BN + half * COLS + c, v);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) acc[c + i] = fmaf(sa * sbp[c + i], v[i], acc[c + i]);
+            for (int i = 0; i < 32; i += 4) {
+              float4 sb4 = hasb ? *reinterpret_cast<const float4*>(sbp + c + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+              fma2_scaled(acc[c + i], acc[c + i + 1], sa, sb4.x, sb4.y, v[i], v[i + 1]);
+              fma2_scaled(acc[c + i + 2], acc[c + i + 3], sa, sb4.z, sb4.w, v[i + 2], v[i + 3]);
+            }
           }
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[buf]);
+          if (lane == 0) {
+            mbar_arrive(&tempty[buf]);
+            mbar_arrive(&sempty[slot]);
+          }
           ++chunk_ctr;
         }
       }
@@ -517,10 +563,11 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.sfb = b.scales_mma;
   p.sfa_kg = a.sf_kpad / 4;
   p.sfb_kg = b.sf_kpad / 4;
-  p.mta = (MBS && a.mant_t) ? a.mant_t : nullptr;
-  p.mtb = (MBS && b.mant_t) ? b.mant_t : nullptr;
-  p.mta_ld = a.mant_t_ld;
-  p.mtb_ld = b.mant_t_ld;
+  const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
+  p.sga = (MBS && ma) ? a.sig_t : nullptr;
+  p.sgb = (MBS && mbb) ? b.sig_t : nullptr;
+  p.sga_ld = a.sig_t_ld;
+  p.sgb_ld = b.sig_t_ld;
   p.tsa = a.variant == NVFP4 ? a.tensor_scale : nullptr;
   p.tsb = b.variant == NVFP4 ? b.tensor_scale : nullptr;
   p.c = c;
@@ -552,12 +599,12 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
   if (a.rows > (1 << 30) || b.rows > (1 << 30) || a.cols > (1 << 30)) return set_error(ERR_UNSUPPORTED, "shape too large");
   if (mbs) {
     const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
-    if ((ma && !a.mant_t) || (mb && !b.mant_t)) return set_error(ERR_INVALID, "MBS operand needs transposed mantissas");
+    if ((ma && !a.sig_t) || (mb && !b.sig_t)) return set_error(ERR_INVALID, "MBS operand needs transposed mantissas");
     const int macro = ma ? a.macro_size : b.macro_size;
     if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
     if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
-    if (c_dtype == MXQ_BF16) return launch_variant<128, 6, 3, false, true, true>(a, b, c, ldc, true, st);
-    return launch_variant<128, 6, 3, false, true, false>(a, b, c, ldc, true, st);
+    if (c_dtype == MXQ_BF16) return launch_variant<128, 5, 3, false, true, true>(a, b, c, ldc, true, st);
+    return launch_variant<128, 5, 3, false, true, false>(a, b, c, ldc, true, st);
   }
   if (sf32) {
     if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, true, false, true>(a, b, c, ldc, true, st);

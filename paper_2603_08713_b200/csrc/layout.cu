@@ -27,28 +27,28 @@ __global__ void k_build_sf(QDesc q, int sf_block, int64_t rows_pad) {
   }
 }
 
-__global__ void k_transpose_m8(QDesc q, int64_t nmac) {
-  const int64_t total = nmac * q.mant_t_ld;
+__global__ void k_sigma_t(QDesc q, int64_t nmac) {
+  const int64_t total = nmac * q.sig_t_ld;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t m = i / q.mant_t_ld, r = i - m * q.mant_t_ld;
-    q.mant_t[i] = r < q.rows ? q.mant[r * q.mant_ld + m] : (uint8_t)0;
+    const int64_t m = i / q.sig_t_ld, r = i - m * q.sig_t_ld;
+    q.sig_t[i] = r < q.rows ? 1.0f / mbs_factor(q.mant[r * q.mant_ld + m]) : 0.0f;
   }
 }
 
 int launch_build_gemm_layout(const QDesc& q, int sf_block, cudaStream_t st) {
-  const int64_t rows_pad = (q.rows + 127) / 128 * 128;
+  const int64_t rows_pad = (q.rows + 255) / 256 * 256;
   if (q.scales_mma) {
     const int64_t total = rows_pad * q.sf_kpad;
     int64_t g = (total + 255) / 256;
     if (g > 4096) g = 4096;
     k_build_sf<<<(unsigned)g, 256, 0, st>>>(q, sf_block, rows_pad);
   }
-  if (q.mant_t && q.mant) {
+  if (q.sig_t && q.mant) {
     const int64_t nmac = (q.cols + q.macro_size - 1) / q.macro_size;
-    const int64_t total = nmac * q.mant_t_ld;
+    const int64_t total = nmac * q.sig_t_ld;
     int64_t g = (total + 255) / 256;
     if (g > 4096) g = 4096;
-    k_transpose_m8<<<(unsigned)g, 256, 0, st>>>(q, nmac);
+    k_sigma_t<<<(unsigned)g, 256, 0, st>>>(q, nmac);
   }
   return check_launch();
 }

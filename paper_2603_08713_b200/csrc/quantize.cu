@@ -144,7 +144,7 @@ __device__ __forceinline__ void store_mbs_outputs(const QDesc& q, int64_t r, int
 
 __device__ __forceinline__ void store_m8(const QDesc& q, int64_t r, int64_t mac, uint8_t m8) {
   if (q.mant) q.mant[r * q.mant_ld + mac] = m8;
-  if (q.mant_t) q.mant_t[mac * q.mant_t_ld + r] = m8;
+  if (q.sig_t) q.sig_t[mac * q.sig_t_ld + r] = 1.0f / mbs_factor(m8);
 }
 
 // Quantise one block (v, scaled by the f32 factor f) with OAS: the shared

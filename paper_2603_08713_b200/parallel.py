@@ -1,0 +1,92 @@
+"""Multi-GPU sharding of the quantize-and-GEMM path (one process per GPU).
+
+Linear layers shard by OUTPUT COLUMN (rows of the weight W[N, K]): every rank
+quantizes its own weight shard once (weights never move), quantizes the
+replicated activation locally (row-independent, so every rank produces the
+same bits), runs the tcgen05 GEMM on its N/world columns and -- only when the
+caller needs the full product -- gathers the output shards with one NCCL
+all_gather over NVLink (SURVEY §8 e, config 4).  Whole-model weight
+quantization shards by layer with no collective (config 3).  NVFP4 is the
+one variant whose quantization couples rows (global amax, src/quantize.py:671):
+``global_amax`` is an all_reduce(MAX) of one scalar.
+
+The collective / assembly logic is written against ``torch.distributed`` and
+plain tensors so it is exercised on CPU with the gloo backend
+(tests/test_parallel_gloo.py); the compute callback is the GPU GEMM in
+production.
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import torch
+import torch.distributed as dist
+
+
+def shard_bounds(n: int, world: int, rank: int, align: int = 128) -> tuple[int, int]:
+    """[lo, hi) rows of an N-row weight owned by `rank`: contiguous, each
+    shard a multiple of `align` rows except possibly the last (so the GEMM's
+    128-row tiles never straddle ranks)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    blocks = -(-n // align)
+    per = blocks // world
+    extra = blocks % world
+    start_blk = rank * per + min(rank, extra)
+    nblk = per + (1 if rank < extra else 0)
+    lo = min(n, start_blk * align)
+    hi = min(n, (start_blk + nblk) * align)
+    return lo, hi
+
+
+def layer_owner(num_layers: int, world: int) -> list[int]:
+    """Layer -> rank for layer-sharded weight quantization (contiguous blocks)."""
+    return [min(world - 1, (l * world) // num_layers) for l in range(num_layers)]
+
+
+def gather_columns(local: torch.Tensor, n_total: int, world: int, group=None) -> torch.Tensor:
+    """All-gather column shards (M, n_r) into the full (M, N) output.
+
+    Shards follow ``shard_bounds``; unequal shards are padded to the largest
+    so one ``all_gather_into_tensor`` suffices, then trimmed and concatenated.
+    """
+    m = local.shape[0]
+    sizes = [shard_bounds(n_total, world, r)[1] - shard_bounds(n_total, world, r)[0] for r in range(world)]
+    width = max(sizes)
+    send = local
+    if local.shape[1] != width:
+        send = torch.zeros((m, width), dtype=local.dtype, device=local.device)
+        send[:, : local.shape[1]] = local
+    flat = torch.empty((world * m, width), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(flat, send.contiguous(), group=group)
+    buf = flat.view(world, m, width)
+    return torch.cat([buf[r, :, : sizes[r]] for r in range(world)], dim=1)
+
+
+def column_sharded_linear(x, w_shard, n_total: int, gemm: Callable, world: int, gather: bool = True,
+                          group=None) -> torch.Tensor:
+    """y = x @ W^T with W split by rows across ranks.  `gemm(x, w_shard)`
+    computes the local (M, n_r) block; the full output is gathered when
+    `gather` (the only data-path collective)."""
+    local = gemm(x, w_shard)
+    if not gather or world == 1:
+        return local
+    return gather_columns(local, n_total, world, group=group)
+
+
+def global_amax(local_amax: torch.Tensor, group=None) -> torch.Tensor:
+    """NVFP4's tensor-wide |x| max across row shards: all_reduce(MAX)."""
+    t = local_amax.clone()
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    """Timing reduction: every multi-GPU time is the max over ranks."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

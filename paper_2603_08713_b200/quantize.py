@@ -284,7 +284,7 @@ class QuantizedTensor:
         q = self.qt()
         q.codes, q.codes_ld = codes.data_ptr(), codes.stride(0)
         pre = self._cache.get(("mma", sf_block))
-        rows_pad = _round_up(rows, 128)
+        rows_pad = _round_up(rows, 256)
         kpad = _round_up(cols, 256) // sf_block
         if pre is not None:
             sf = pre
@@ -294,23 +294,23 @@ class QuantizedTensor:
         keep.append(sf)
         mt = None
         if self.mbs_mantissas is not None:
-            mt = self._cache.get("mant_t")
+            mt = self._cache.get("sig_t")
             if mt is None:
-                mt = torch.empty((self.n_macros, rows_pad), dtype=torch.uint8, device=dev)
-            q.mant_t, q.mant_t_ld = mt.data_ptr(), mt.stride(0)
+                mt = torch.empty((self.n_macros, rows_pad), dtype=torch.float32, device=dev)
+            q.sig_t, q.sig_t_ld = mt.data_ptr(), mt.stride(0)
             keep.append(mt)
         need_sf = pre is None
-        need_mt = self.mbs_mantissas is not None and self._cache.get("mant_t") is None
+        need_mt = self.mbs_mantissas is not None and self._cache.get("sig_t") is None
         if need_sf or need_mt:
             qb = _lib.QT.from_buffer_copy(q)
             if not need_sf:
                 qb.scales_mma = None
             if not need_mt:
-                qb.mant_t = None
+                qb.sig_t = None
             _lib.check(_lib.lib().mxq_build_gemm_layout(ctypes.byref(qb), sf_block, stream), "build_gemm_layout")
             self._cache[("mma", sf_block)] = sf
             if mt is not None:
-                self._cache["mant_t"] = mt
+                self._cache["sig_t"] = mt
         ts = self._ts_device()
         if ts is not None:
             keep.append(ts)
@@ -460,14 +460,14 @@ class _Outputs:
         self.codes_buf = torch.empty((rows, _round_up(cols // 2, 16)), dtype=torch.uint8, device=dev)
         self.codes = self.codes_buf[:, : cols // 2]
         self.scales = torch.empty((rows, cols // bs), dtype=torch.uint8, device=dev)
-        self.rows_pad = _round_up(rows, 128)
+        self.rows_pad = _round_up(rows, 256)
         self.kpad = _round_up(cols, 256) // bs
         self.sf_mma = (torch.empty(self.rows_pad * self.kpad, dtype=torch.uint8, device=dev)
                        if gemm_layout else None)
         mbs = variant in MBS_VARIANTS
         nmac = -(-cols // macro)
         self.mant = torch.empty((rows, nmac), dtype=torch.uint8, device=dev) if mbs else None
-        self.mant_t = (torch.empty((nmac, self.rows_pad), dtype=torch.uint8, device=dev)
+        self.sig_t = (torch.empty((nmac, self.rows_pad), dtype=torch.float32, device=dev)
                        if (mbs and gemm_layout) else None)
         self.ts = torch.empty(1, dtype=torch.float64, device=dev) if variant is Variant.NVFP4 else None
         self.status = torch.zeros(4, dtype=torch.int32, device=dev)
@@ -482,8 +482,8 @@ class _Outputs:
             q.scales_mma, q.sf_kpad = self.sf_mma.data_ptr(), self.kpad
         if self.mant is not None:
             q.mant, q.mant_ld = self.mant.data_ptr(), self.mant.stride(0)
-        if self.mant_t is not None:
-            q.mant_t, q.mant_t_ld = self.mant_t.data_ptr(), self.mant_t.stride(0)
+        if self.sig_t is not None:
+            q.sig_t, q.sig_t_ld = self.sig_t.data_ptr(), self.sig_t.stride(0)
         if self.ts is not None:
             q.tensor_scale = self.ts.data_ptr()
         return q
@@ -537,8 +537,8 @@ def quantize_tensor(t, cfg: SchemeConfig, *, check: bool = True, gemm_layout: bo
     c["status"] = out.status
     if out.sf_mma is not None:
         c[("mma", bs)] = out.sf_mma
-    if out.mant_t is not None:
-        c["mant_t"] = out.mant_t
+    if out.sig_t is not None:
+        c["sig_t"] = out.sig_t
     if nv:
         c["ts"] = out.ts
     return res
