@@ -180,14 +180,40 @@ def run_ours(args):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    def time_steps(arm, k, w):
-        for _ in range(w):
+    graphs = {}
+
+    def capture(arm):
+        """The whole step (4 x quantize + GEMM [+ all_gather]) as one CUDA graph."""
+        if world > 1:
+            return None  # NCCL collectives are replayed eagerly
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            step(arm)  # warm (allocations, attributes, descriptors)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
             step(arm)
+        return g
+
+    def run_step(arm):
+        g = graphs.get(arm)
+        if g is not None:
+            g.replay()
+        else:
+            step(arm)
+
+    def time_steps(arm, k, w):
+        if args.graphs and arm not in graphs:
+            graphs[arm] = capture(arm)
+        for _ in range(w):
+            run_step(arm)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(k):
-            step(arm)
+            run_step(arm)
         e1.record()
         barrier()
         ms = e0.elapsed_time(e1) / k
@@ -224,19 +250,34 @@ def run_ours(args):
     # ---- quantizer bandwidth (4096x4096 bf16 activation, one launch) -------
     qbw = {}
     x = acts[0]
+    # algorithmic bytes / element: bf16 read + packed codes + scale bytes
+    # (+ MBS mantissa byte per 128 elements); the GEMM-layout copies the
+    # kernels also write (row-major + MMA-atom scales, f32 sigma) are not
+    # counted, so the GB/s is conservative.
     bytes_per_el = {"ocp32": 2 + 0.5 + 1 / 32, "mx16": 2 + 0.5 + 1 / 16, "mx16_oas": 2 + 0.5 + 1 / 16,
                     "mbs_s": 2 + 0.5 + 1 / 16 + 1 / 128, "mbs_d": 2 + 0.5 + 1 / 16 + 1 / 128,
                     "nvfp4": 2 + 0.5 + 1 / 16}
     for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "nvfp4", "mbs_d"):
         cfg = M.SchemeConfig(V(vname))
-        reps = 5 if vname == "mbs_d" else 20
+        reps = 5 if vname == "mbs_d" else 50
         for _ in range(3):
-            M.quantize_tensor(x, cfg, check=False, gemm_layout=False)
+            M.quantize_tensor(x, cfg, check=False, gemm_layout=True)
         torch.cuda.synchronize()
+        g = None
+        if args.graphs and vname != "mbs_d":  # MBS-D uploads its candidate table per call
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(reps):
+                    M.quantize_tensor(x, cfg, check=False, gemm_layout=True)
+            g.replay()
+            torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(reps):
-            M.quantize_tensor(x, cfg, check=False, gemm_layout=False)
+        if g is not None:
+            g.replay()
+        else:
+            for _ in range(reps):
+                M.quantize_tensor(x, cfg, check=False, gemm_layout=True)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
@@ -450,6 +491,8 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-wrows", type=int, default=2048)
+    ap.add_argument("--no-graphs", dest="graphs", action="store_false",
+                    help="launch every kernel eagerly instead of replaying a captured CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -36,9 +36,7 @@ constexpr int BM = 128;
 constexpr int KSTAGE = 256;            // elements per pipeline stage
 constexpr int KSTEP = 64;              // elements per tcgen05.mma (FP4, K64)
 constexpr int STAGE_BYTES_A = BM * KSTAGE / 2;  // 16 KB
-constexpr int NUM_THREADS = 384;       // 4 control warps + 8 epilogue warps
-constexpr int EPI_WARP0 = 4;
-constexpr int NUM_EPI_WARPS = 8;
+constexpr int EPI_WARP0 = 4;           // warps 0-3: TMA, MMA, sigma producer, spare
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -177,8 +175,31 @@ __device__ __forceinline__ void fma2_scaled(float& acc0, float& acc1, float sa, 
       : "f"(sb0), "f"(sb1), "f"(p0), "f"(p1), "f"(sa));
 }
 
-__device__ __forceinline__ void epi_bar_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32) : "memory");
+// 32 lanes x 16 columns.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void mul2(float& o0, float& o1, float a, float b0, float b1) {
+  asm("{\n\t.reg .b64 x, y;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %4};\n\t"
+      "mul.rn.f32x2 x, x, y;\n\tmov.b64 {%0, %1}, x;\n\t}"
+      : "=f"(o0), "=f"(o1)
+      : "f"(b0), "f"(b1), "f"(a));
+}
+
+__device__ __forceinline__ void fma2(float& acc0, float& acc1, float w0, float w1, float p0, float p1) {
+  asm("{\n\t.reg .b64 w, q, c;\n\tmov.b64 w, {%2, %3};\n\tmov.b64 q, {%4, %5};\n\t"
+      "mov.b64 c, {%0, %1};\n\tfma.rn.f32x2 c, w, q, c;\n\tmov.b64 {%0, %1}, c;\n\t}"
+      : "+f"(acc0), "+f"(acc1)
+      : "f"(w0), "f"(w1), "f"(p0), "f"(p1));
 }
 
 // ---------------------------------------------------------------------------
@@ -225,12 +246,17 @@ struct Cfg {
   static constexpr int COL_SF = NB * BN;
   static constexpr int TMEM_COLS_USED = COL_SF + 2 * (SFA_COLS + SFB_COLS);
   static constexpr int TMEM_COLS = 512;
+  // MBS: 16 epilogue warps (4 per TMEM lane quadrant, 32 columns each) to hide
+  // the per-chunk latency chain; plain: 8 warps (2 per quadrant).
+  static constexpr int EPIW = MBS ? 16 : 8;
+  static constexpr int THREADS = (EPI_WARP0 + EPIW) * 32;
+  static constexpr int COLS = BN / (EPIW / 4);
   static_assert(TMEM_COLS_USED <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
 template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
   using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
   extern __shared__ uint8_t smem_raw[];
@@ -256,11 +282,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], NUM_EPI_WARPS);
+      mbar_init(&tempty[b], C::EPIW);
     }
     for (int b = 0; b < C::NSIG; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&sempty[b], NUM_EPI_WARPS);
+      mbar_init(&sempty[b], C::EPIW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -385,10 +411,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= EPI_WARP0) {
     // ===================== epilogue =====================
-    const int e = warp - EPI_WARP0;        // 0..7
+    const int e = warp - EPI_WARP0;
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
-    const int half = e >> 2;               // column half
-    constexpr int COLS = BN / 2;           // columns per thread
+    const int half = e >> 2;               // column part (0 .. EPIW/4-1)
+    constexpr int COLS = C::COLS;          // columns per thread
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     uint32_t chunk_ctr = 0;
@@ -416,35 +442,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (lane == 0) mbar_arrive(&tempty[buf]);
         ++chunk_ctr;
       } else {
+        static_assert(COLS == 32, "MBS epilogue: 32 columns per thread");
 #pragma unroll
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
+        const bool hasa = p.sga != nullptr, hasb = p.sgb != nullptr;
         for (int t = 0; t < p.n_chunks; ++t) {
+          // (1) sigma for this chunk (landed long ago): w_j = sigmaA_i * sigmaB_j,
+          //     computed before the partial product is waited for.
           const uint32_t slot = chunk_ctr % C::NSIG;
           mbar_wait(&sfull[slot], (chunk_ctr / C::NSIG) & 1);
           const float* sig = reinterpret_cast<const float*>(smem + C::OFF_SIG + slot * C::SIG_SLOT);
-          const float sa = p.sga ? sig[row_in_tile] : 1.0f;
+          const float sa = hasa ? sig[row_in_tile] : 1.0f;
           const float* sbp = sig + BM + half * COLS;
-          const bool hasb = p.sgb != nullptr;
+          float w[COLS];
+#pragma unroll
+          for (int i = 0; i < COLS; i += 4) {
+            const float4 sb4 = hasb ? *reinterpret_cast<const float4*>(sbp + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+            mul2(w[i], w[i + 1], sa, sb4.x, sb4.y);
+            mul2(w[i + 2], w[i + 3], sa, sb4.z, sb4.w);
+          }
+          // (2) the chunk's partial P from TMEM; the buffer is released as soon
+          //     as it is in registers, so the MMA runs ahead during the FMAs.
           const uint32_t buf = chunk_ctr % NB;
           mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
           tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < COLS; c += 32) {
-            float v[32];
-            tmem_ld32(tmem + lane_addr + buf * BN + half * COLS + c, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 sb4 = hasb ? *reinterpret_cast<const float4*>(sbp + c + i) : make_float4(1.f, 1.f, 1.f, 1.f);
-              fma2_scaled(acc[c + i], acc[c + i + 1], sa, sb4.x, sb4.y, v[i], v[i + 1]);
-              fma2_scaled(acc[c + i + 2], acc[c + i + 3], sa, sb4.z, sb4.w, v[i + 2], v[i + 3]);
-            }
-          }
+          float v0[16], v1[16];
+          tmem_ld16(tmem + lane_addr + buf * BN + half * COLS, v0);
+          tmem_ld16(tmem + lane_addr + buf * BN + half * COLS + 16, v1);
+          tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
             mbar_arrive(&tempty[buf]);
             mbar_arrive(&sempty[slot]);
+          }
+          // (3) acc += w * P  (FFMA2)
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            fma2(acc[i], acc[i + 1], w[i], w[i + 1], v0[i], v0[i + 1]);
+            fma2(acc[16 + i], acc[16 + i + 1], w[16 + i], w[16 + i + 1], v1[i], v1[i + 1]);
           }
           ++chunk_ctr;
         }
@@ -581,7 +617,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.idesc = make_idesc(BN, ue8m0);
   const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, NUM_THREADS, C::SMEM, st>>>(ta, tb, p);
+  kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, p);
   return check_launch();
 }
 

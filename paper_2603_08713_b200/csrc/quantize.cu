@@ -95,26 +95,185 @@ __device__ __forceinline__ void store_scale(const QDesc& q, int64_t r, int64_t k
 }
 
 // ---------------------------------------------------------------------------
-// K1: power-of-two variants.  Grid-stride over blocks; thread == block.
+// Streaming fast path (K1, K2).  Index math uses a precomputed 32-bit
+// division (the 64-bit integer division the first version used cost ~100
+// instructions per block); the -0 fix-up, absmax and scaling run on packed
+// words; every thread keeps two blocks of loads in flight.
 // ---------------------------------------------------------------------------
-template <int BS, bool OCP, bool OAS>
-__global__ void __launch_bounds__(256) k_quantize_pow2(const void* __restrict__ x, int dtype, int64_t x_ld,
-                                                       QDesc q, uint32_t* __restrict__ status) {
-  const int64_t nbr = q.cols / BS;
-  const int64_t nb = q.rows * nbr;
+struct FastDiv {
+  uint32_t d, m, s;
+};
+
+static FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  f.s = 0;
+  while ((1ull << f.s) < d) ++f.s;
+  f.m = (uint32_t)((((1ull << 32) * ((1ull << f.s) - d)) / d) + 1);
+  return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  return (uint32_t)(((uint64_t)__umulhi(n, f.m) + n) >> f.s);
+}
+
+// Clear the sign bit of every nibble whose magnitude is 0 (the reference maps
+// -0 / negative flushes to code 0): mag + 7 carries into bit 3 iff mag != 0.
+__device__ __forceinline__ uint32_t fix_neg_zero(uint32_t w) {
+  const uint32_t nz = ((w & 0x77777777u) + 0x77777777u) & 0x88888888u;
+  return w & (0x77777777u | nz);
+}
+
+__device__ __forceinline__ uint32_t cvt_e2m1x2(float lo, float hi) {
+  uint16_t r;
+  asm("{\n\t.reg .b8 t;\n\tcvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n\tcvt.u16.u8 %0, t;\n\t}" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__device__ __forceinline__ void fmul2(float& o0, float& o1, float a0, float a1, float s) {
+  asm("{\n\t.reg .b64 x, y;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %4};\n\t"
+      "mul.rn.f32x2 x, x, y;\n\tmov.b64 {%0, %1}, x;\n\t}"
+      : "=f"(o0), "=f"(o1) : "f"(a0), "f"(a1), "f"(s));
+}
+
+// 16 raw elements of one block.
+template <int DT>
+struct Blk16 {
+  uint32_t w[DT == DT_BF16 ? 8 : 16];
+};
+
+template <int DT>
+__device__ __forceinline__ void ld_blk(const void* __restrict__ x, int64_t off, Blk16<DT>& b) {
+  if constexpr (DT == DT_BF16) {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + off);
+    const uint4 a0 = __ldcs(p), a1 = __ldcs(p + 1);
+    b.w[0] = a0.x; b.w[1] = a0.y; b.w[2] = a0.z; b.w[3] = a0.w;
+    b.w[4] = a1.x; b.w[5] = a1.y; b.w[6] = a1.z; b.w[7] = a1.w;
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(x) + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 a = __ldcs(p + q);
+      b.w[4 * q] = a.x; b.w[4 * q + 1] = a.y; b.w[4 * q + 2] = a.z; b.w[4 * q + 3] = a.w;
+    }
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void zero_blk(Blk16<DT>& b) {
+#pragma unroll
+  for (int i = 0; i < (DT == DT_BF16 ? 8 : 16); ++i) b.w[i] = 0u;
+}
+
+// |x| max as f32 (exact), and the non-finite flag: integer max of the
+// sign-cleared bit patterns (ordering of non-negative floats; NaN/Inf sort
+// above every finite value).
+template <int DT>
+__device__ __forceinline__ float blk_absmax(const Blk16<DT>& b, uint32_t& bad) {
+  if constexpr (DT == DT_BF16) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m = __vmaxu2(m, b.w[j] & 0x7FFF7FFFu);
+    const uint32_t top = max(m & 0xFFFFu, m >> 16);
+    bad |= (top >= 0x7F80u) ? 1u : 0u;
+    return __uint_as_float(top << 16);
+  } else {
+    uint32_t m = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) m = max(m, b.w[j] & 0x7FFFFFFFu);
+    bad |= (m >= 0x7F800000u) ? 1u : 0u;
+    return __uint_as_float(m);
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ void blk_f32(const Blk16<DT>& b, float (&v)[16]) {
+  if constexpr (DT == DT_BF16) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      v[2 * j] = __uint_as_float(b.w[j] << 16);
+      v[2 * j + 1] = __uint_as_float(b.w[j] & 0xFFFF0000u);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(b.w[j]);
+  }
+}
+
+// 16 codes of v * sf (exact power-of-two scaling) -> two packed words.
+__device__ __forceinline__ void enc16(const float (&v)[16], float sf, uint32_t (&out)[2]) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float lo, hi;
+      fmul2(lo, hi, v[8 * h + 2 * j], v[8 * h + 2 * j + 1], sf);
+      word |= cvt_e2m1x2(lo, hi) << (8 * j);
+    }
+    out[h] = fix_neg_zero(word);
+  }
+}
+
+__device__ __forceinline__ void store_scale(const QDesc& q, uint32_t r, uint32_t kb, uint8_t s) {
+  if (q.scales) q.scales[(int64_t)r * q.scales_ld + kb] = s;
+  if (q.scales_mma) q.scales_mma[sf_mma_offset(r, kb, q.sf_kpad)] = s;
+}
+
+// One 16-block of MX16 / MX16_OAS.
+template <int DT, bool OAS>
+__device__ __forceinline__ void do_blk16(const Blk16<DT>& b, const QDesc& q, uint32_t r, uint32_t kb,
+                                         uint32_t& bad) {
+  const float alpha = blk_absmax<DT>(b, bad);
+  const uint8_t biased = e8m0_biased_16(alpha, OAS);
+  float v[16];
+  blk_f32<DT>(b, v);
+  uint32_t codes[2];
+  enc16(v, exp2i_f32(127 - (int)biased), codes);
+  *reinterpret_cast<uint2*>(q.codes + (int64_t)r * q.codes_ld + kb * 8) = make_uint2(codes[0], codes[1]);
+  store_scale(q, r, kb, biased);
+}
+
+// K1a: MX16 / MX16_OAS (block 16).  Thread = two blocks per iteration.
+template <int DT, bool OAS>
+__global__ void __launch_bounds__(256) k_quantize_mx16(const void* __restrict__ x, int64_t x_ld, QDesc q,
+                                                       FastDiv fd_nbr, uint32_t nb, uint32_t* __restrict__ status) {
   uint32_t bad = 0;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = b / nbr, kb = b - r * nbr;
-    float v[BS];
-    load_block<BS>(x, dtype, r * x_ld + kb * BS, v);
-    bool fin;
-    float alpha = block_absmax<BS>(v, fin);
-    bad |= !fin;
-    uint8_t biased = OCP ? e8m0_biased_ocp(alpha) : e8m0_biased_16(alpha, OAS);
-    float sf = exp2i_f32(127 - (int)biased);
-    uint32_t packed[BS / 8];
-    encode_block<BS>(v, sf, packed);
-    store_codes<BS>(q.codes + r * q.codes_ld + kb * (BS / 2), packed);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t b0 = blockIdx.x * blockDim.x + threadIdx.x; b0 < nb; b0 += 2 * stride) {
+    const uint32_t b1 = b0 + stride;
+    const uint32_t r0 = fdiv(b0, fd_nbr), k0 = b0 - r0 * fd_nbr.d;
+    const uint32_t r1 = fdiv(b1, fd_nbr), k1 = b1 - r1 * fd_nbr.d;
+    Blk16<DT> x0, x1;
+    ld_blk<DT>(x, (int64_t)r0 * x_ld + k0 * 16, x0);
+    if (b1 < nb) ld_blk<DT>(x, (int64_t)r1 * x_ld + k1 * 16, x1);
+    do_blk16<DT, OAS>(x0, q, r0, k0, bad);
+    if (b1 < nb) do_blk16<DT, OAS>(x1, q, r1, k1, bad);
+  }
+  if (bad) atomicOr(status, ST_NONFINITE);
+}
+
+// K1b: OCP32 (block 32 = two 16-element halves sharing one scale).
+template <int DT>
+__global__ void __launch_bounds__(256) k_quantize_ocp32(const void* __restrict__ x, int64_t x_ld, QDesc q,
+                                                        FastDiv fd_nbr, uint32_t nb, uint32_t* __restrict__ status) {
+  uint32_t bad = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
+    const uint32_t r = fdiv(b, fd_nbr), kb = b - r * fd_nbr.d;
+    Blk16<DT> h0, h1;
+    ld_blk<DT>(x, (int64_t)r * x_ld + kb * 32, h0);
+    ld_blk<DT>(x, (int64_t)r * x_ld + kb * 32 + 16, h1);
+    const float alpha = fmaxf(blk_absmax<DT>(h0, bad), blk_absmax<DT>(h1, bad));
+    const uint8_t biased = e8m0_biased_ocp(alpha);
+    const float sf = exp2i_f32(127 - (int)biased);
+    float v[16];
+    uint32_t c0[2], c1[2];
+    blk_f32<DT>(h0, v);
+    enc16(v, sf, c0);
+    blk_f32<DT>(h1, v);
+    enc16(v, sf, c1);
+    *reinterpret_cast<uint4*>(q.codes + (int64_t)r * q.codes_ld + kb * 16) = make_uint4(c0[0], c0[1], c1[0], c1[1]);
     store_scale(q, r, kb, biased);
   }
   if (bad) atomicOr(status, ST_NONFINITE);
@@ -123,7 +282,7 @@ __global__ void __launch_bounds__(256) k_quantize_pow2(const void* __restrict__ 
 // ---------------------------------------------------------------------------
 // Macro-group geometry for MBS: G lanes (a power of two <= 32) own one macro
 // of up to 32 blocks (macro_size <= 512); a trailing partial macro simply has
-// fewer active lanes.  `gid` enumerates (row, macro) pairs.
+// fewer active lanes.
 // ---------------------------------------------------------------------------
 struct MacroGeom {
   int G;          // lanes per macro group
@@ -136,72 +295,65 @@ __device__ __forceinline__ float group_max(float v, int G) {
   return v;
 }
 
-__device__ __forceinline__ void store_mbs_outputs(const QDesc& q, int64_t r, int64_t mac, int64_t kb,
-                                                  const uint32_t (&packed)[2], uint8_t biased) {
-  store_codes<16>(q.codes + r * q.codes_ld + kb * 8, packed);
-  store_scale(q, r, kb, biased);
-}
-
 __device__ __forceinline__ void store_m8(const QDesc& q, int64_t r, int64_t mac, uint8_t m8) {
   if (q.mant) q.mant[r * q.mant_ld + mac] = m8;
   if (q.sig_t) q.sig_t[mac * q.sig_t_ld + r] = 1.0f / mbs_factor(m8);
 }
 
 // Quantise one block (v, scaled by the f32 factor f) with OAS: the shared
-// second half of MBS-S and MBS-D (src/quantize.py:392-406).
-__device__ __forceinline__ uint8_t mbs_block(const float (&v)[16], float f, uint32_t (&packed)[2], bool& ovf) {
+// second half of MBS-S and MBS-D (src/quantize.py:392-406).  y = RN(x*f);
+// max|y| = RN(max|x| * f) because rounding is monotone.
+__device__ __forceinline__ uint8_t mbs_block(const float (&v)[16], float alpha, float f, uint32_t (&packed)[2],
+                                             bool& ovf) {
   float y[16];
-  float a = 0.0f;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    y[i] = __fmul_rn(v[i], f);
-    a = fmaxf(a, fabsf(y[i]));
-  }
+  for (int i = 0; i < 16; i += 2) fmul2(y[i], y[i + 1], v[i], v[i + 1], f);
+  const float a = __fmul_rn(alpha, f);
   ovf = !(a <= 3.402823466e38f);
-  uint8_t biased = e8m0_biased_16(a, true);
-  encode_block<16>(y, exp2i_f32(127 - (int)biased), packed);
+  const uint8_t biased = e8m0_biased_16(a, true);
+  enc16(y, exp2i_f32(127 - (int)biased), packed);
   return biased;
 }
 
 // K2: MBS-Static.  The CTA-uniform `base` loop keeps every warp converged
 // for the group shuffles.
-__global__ void __launch_bounds__(256) k_quantize_mbs_s(const void* __restrict__ x, int dtype, int64_t x_ld,
-                                                        QDesc q, MacroGeom g, uint32_t* __restrict__ status) {
+template <int DT>
+__global__ void __launch_bounds__(256) k_quantize_mbs_s(const void* __restrict__ x, int64_t x_ld, QDesc q,
+                                                        MacroGeom g, FastDiv fd_nmac, uint32_t ngroups,
+                                                        uint32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int sub = lane & (g.G - 1);
-  const int64_t ngroups = q.rows * g.nmac;
-  const int64_t gpb = (int64_t)blockDim.x / g.G;  // groups per CTA pass
-  uint32_t bad = 0;
-  for (int64_t base = (int64_t)blockIdx.x * gpb; base < ngroups; base += (int64_t)gridDim.x * gpb) {
-    const int64_t gi = base + threadIdx.x / g.G;
+  const uint32_t gpb = blockDim.x / g.G;  // groups per CTA pass
+  uint32_t bad = 0, ovf_any = 0;
+  for (uint32_t base = blockIdx.x * gpb; base < ngroups; base += gridDim.x * gpb) {
+    const uint32_t gi = base + threadIdx.x / g.G;
     const bool live_group = gi < ngroups;
-    const int64_t r = live_group ? gi / g.nmac : 0;
-    const int64_t mac = live_group ? gi - r * g.nmac : 0;
-    const int64_t c0 = mac * g.macro + (int64_t)sub * 16;
-    const int64_t width = live_group ? min((int64_t)g.macro, q.cols - mac * g.macro) : 0;
+    const uint32_t r = live_group ? fdiv(gi, fd_nmac) : 0u;
+    const uint32_t mac = live_group ? gi - r * fd_nmac.d : 0u;
+    const int64_t c0 = (int64_t)mac * g.macro + (int64_t)sub * 16;
+    const int64_t width = live_group ? min((int64_t)g.macro, q.cols - (int64_t)mac * g.macro) : 0;
     const bool active = live_group && sub * 16 < width;
-    float v[16];
-    if (active) load_block<16>(x, dtype, r * x_ld + c0, v);
-    else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.0f;
-    }
-    bool fin;
-    float a16 = block_absmax<16>(v, fin);
-    bad |= !fin;
+    Blk16<DT> xb;
+    if (active) ld_blk<DT>(x, (int64_t)r * x_ld + c0, xb);
+    else zero_blk<DT>(xb);
+    const float a16 = blk_absmax<DT>(xb, bad);
     const float amac = group_max(a16, g.G);
     const uint8_t m8 = static_m8(amac);
+    float v[16];
+    blk_f32<DT>(xb, v);
     uint32_t packed[2];
     bool ovf;
-    const uint8_t biased = mbs_block(v, mbs_factor(m8), packed, ovf);
+    const uint8_t biased = mbs_block(v, a16, mbs_factor(m8), packed, ovf);
     if (active) {
-      bad |= ovf ? 2u : 0u;
-      store_mbs_outputs(q, r, mac, c0 / 16, packed, biased);
+      ovf_any |= ovf ? 1u : 0u;
+      const uint32_t kb = (uint32_t)(c0 >> 4);
+      *reinterpret_cast<uint2*>(q.codes + (int64_t)r * q.codes_ld + kb * 8) = make_uint2(packed[0], packed[1]);
+      store_scale(q, r, kb, biased);
       if (sub == 0) store_m8(q, r, mac, m8);
     }
   }
-  if (bad & 1u) atomicOr(status, ST_NONFINITE);
-  if (bad & 2u) atomicOr(status, ST_OVERFLOW);
+  if (bad) atomicOr(status, ST_NONFINITE);
+  if (ovf_any) atomicOr(status, ST_OVERFLOW);
 }
 
 // ---------------------------------------------------------------------------
@@ -365,10 +517,11 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
     const uint32_t m8 = __shfl_sync(0xffffffffu, best_m8, lane & ~(g.G - 1));
     uint32_t packed[2];
     bool ovf;
-    const uint8_t biased = mbs_block(v, mbs_factor(m8), packed, ovf);
+    const uint8_t biased = mbs_block(v, a16, mbs_factor(m8), packed, ovf);
     if (active) {
       bad |= ovf ? 2u : 0u;
-      store_mbs_outputs(q, r, mac, c0 / 16, packed, biased);
+      *reinterpret_cast<uint2*>(q.codes + r * q.codes_ld + (c0 / 16) * 8) = make_uint2(packed[0], packed[1]);
+      store_scale(q, (uint32_t)r, (uint32_t)(c0 / 16), biased);
       if (sub == 0) store_m8(q, r, mac, (uint8_t)m8);
     }
   }
@@ -487,19 +640,29 @@ static int macro_lanes(int macro) {
 int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int mbs_mode, const uint8_t* cand,
                     int n_cand, int augment, uint32_t* status, cudaStream_t st) {
   const int64_t rows = q.rows, cols = q.cols;
+  const int64_t nbr16 = cols / 16;
+  if (rows * nbr16 >= (int64_t)1 << 31) return set_error(ERR_UNSUPPORTED, "tensor too large (>= 2^31 blocks)");
+  const bool bf = dtype == DT_BF16;
   switch (q.variant) {
     case OCP32: {
-      const int64_t nb = rows * (cols / 32);
-      k_quantize_pow2<32, true, false><<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status);
+      const uint32_t nb = (uint32_t)(rows * (cols / 32));
+      const FastDiv fd = make_fastdiv((uint32_t)(cols / 32));
+      if (bf) k_quantize_ocp32<DT_BF16><<<grid_for(nb, 256), 256, 0, st>>>(x, x_ld, q, fd, nb, status);
+      else k_quantize_ocp32<DT_F32><<<grid_for(nb, 256), 256, 0, st>>>(x, x_ld, q, fd, nb, status);
       break;
     }
     case MX16:
     case MX16_OAS: {
-      const int64_t nb = rows * (cols / 16);
-      if (q.variant == MX16)
-        k_quantize_pow2<16, false, false><<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status);
-      else
-        k_quantize_pow2<16, false, true><<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status);
+      const uint32_t nb = (uint32_t)(rows * nbr16);
+      const FastDiv fd = make_fastdiv((uint32_t)nbr16);
+      const int grid = grid_for((nb + 1) / 2, 256);
+      if (q.variant == MX16) {
+        if (bf) k_quantize_mx16<DT_BF16, false><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
+        else k_quantize_mx16<DT_F32, false><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
+      } else {
+        if (bf) k_quantize_mx16<DT_BF16, true><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
+        else k_quantize_mx16<DT_F32, true><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
+      }
       break;
     }
     case MBS_S:
@@ -511,7 +674,10 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
       const int64_t ngroups = rows * g.nmac;
       if (q.variant == MBS_S) {
-        k_quantize_mbs_s<<<grid_for(ngroups * g.G, 256), 256, 0, st>>>(x, dtype, x_ld, q, g, status);
+        const FastDiv fd = make_fastdiv((uint32_t)g.nmac);
+        const int grid = grid_for(ngroups * g.G, 256);
+        if (bf) k_quantize_mbs_s<DT_BF16><<<grid, 256, 0, st>>>(x, x_ld, q, g, fd, (uint32_t)ngroups, status);
+        else k_quantize_mbs_s<DT_F32><<<grid, 256, 0, st>>>(x, x_ld, q, g, fd, (uint32_t)ngroups, status);
       } else {
         if (mbs_mode != 0) return set_error(ERR_INVALID, "mbs_mode='lut' runs through mxq_quantize_mbs_lut");
         if (n_cand < 1 || n_cand > 256) return set_error(ERR_INVALID, "candidate count out of range");
