@@ -92,6 +92,9 @@ int mxq_version(void);
 const char* mxq_last_error(void);
 /* 1 when a CUDA device of compute capability 10.0 is present. */
 int mxq_device_ok(void);
+/* Development aid: device buffer (>= 512*4 int64) for a clock64() trace of
+ * CTA 0's MMA/epilogue hand-offs in subsequent GEMM launches; NULL disables. */
+void mxq_debug_set_trace(long long* dev_buf);
 
 /*
  * Quantize a dense (rows, cols) f32/bf16 device tensor `x` (row stride x_ld

@@ -48,6 +48,7 @@ SIGNATURES = {
     "mxq_version": (ctypes.c_int, []),
     "mxq_last_error": (ctypes.c_char_p, []),
     "mxq_device_ok": (ctypes.c_int, []),
+    "mxq_debug_set_trace": (None, [_P]),
     "mxq_quantize": (ctypes.c_int, [_P, _I32, _I64, _PQT, _I32, _P, _I32, _I32, _P, _P]),
     "mxq_quantize_mbs_lut": (ctypes.c_int, [_P, _I32, _I64, _PQT, _P, _I32, _P, _P, _P]),
     "mxq_dequantize": (ctypes.c_int, [_PQT, _P, _I64, _P, _P]),

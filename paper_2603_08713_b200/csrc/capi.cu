@@ -74,6 +74,10 @@ extern "C" {
 
 int mxq_version(void) { return 100; }
 
+// Development aid: when non-NULL, the next GEMM launches write a clock64()
+// trace of CTA 0's MMA / epilogue hand-offs (4 x int64 per chunk) there.
+void mxq_debug_set_trace(long long* dev_buf) { set_gemm_trace(dev_buf); }
+
 const char* mxq_last_error(void) { return g_err.c_str(); }
 
 int mxq_device_ok(void) {

@@ -220,7 +220,10 @@ struct Params {
   int macro_steps;      // MBS chunk length in 64-K MMA steps
   int n_chunks;         // MBS chunks per tile (== n_macros)
   uint32_t idesc;       // instruction descriptor without scale-factor ids
+  long long* trace;     // optional clock64 trace of CTA 0 (mxq_debug_set_trace)
 };
+
+constexpr int TRACE_CHUNKS = 512;
 
 template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
 struct Cfg {
@@ -366,8 +369,10 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
               if (in_chunk == 0) {
                 if (open) tc_commit(&tfull[buf]);
                 buf = chunk_ctr % NB;
+                if (p.trace && blockIdx.x == 0 && chunk_ctr < TRACE_CHUNKS) p.trace[chunk_ctr * 4 + 0] = clock64();
                 mbar_wait(&tempty[buf], ((chunk_ctr / NB) & 1) ^ 1);
                 tc_fence_after();
+                if (p.trace && blockIdx.x == 0 && chunk_ctr < TRACE_CHUNKS) p.trace[chunk_ctr * 4 + 1] = clock64();
                 ++chunk_ctr;
                 open = true;
               }
@@ -464,8 +469,11 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
           // (2) the chunk's partial P from TMEM; the buffer is released as soon
           //     as it is in registers, so the MMA runs ahead during the FMAs.
           const uint32_t buf = chunk_ctr % NB;
+          const bool tr = p.trace && blockIdx.x == 0 && e == 0 && lane == 0 && chunk_ctr < TRACE_CHUNKS;
+          if (tr) p.trace[chunk_ctr * 4 + 2] = clock64();
           mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
           tc_fence_after();
+          if (tr) p.trace[chunk_ctr * 4 + 3] = clock64();
           float v0[16], v1[16];
           tmem_ld16(tmem + lane_addr + buf * BN + half * COLS, v0);
           tmem_ld16(tmem + lane_addr + buf * BN + half * COLS + 16, v1);
@@ -579,6 +587,8 @@ static uint32_t make_idesc(int n, bool ue8m0) {
   return d;
 }
 
+static long long* g_trace = nullptr;
+
 template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
 static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, bool ue8m0, cudaStream_t st) {
   using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
@@ -615,6 +625,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.macro_steps = macro / KSTEP;
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.idesc = make_idesc(BN, ue8m0);
+  p.trace = g_trace;
   const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, p);
@@ -622,6 +633,8 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
 }
 
 }  // namespace tc
+
+void set_gemm_trace(long long* p) { tc::g_trace = p; }
 
 int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, uint32_t* status,
                    cudaStream_t st) {
