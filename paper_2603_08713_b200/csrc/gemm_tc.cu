@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
@@ -36,7 +37,12 @@ constexpr int BM = 128;
 constexpr int KSTAGE = 256;            // elements per pipeline stage
 constexpr int KSTEP = 64;              // elements per tcgen05.mma (FP4, K64)
 constexpr int STAGE_BYTES_A = BM * KSTAGE / 2;  // 16 KB
-constexpr int EPI_WARP0 = 4;           // warps 0-3: TMA, MMA, sigma producer, spare
+// Warp roles.  The SM's warp arbiter issues highest-warp-id first, so the
+// latency-critical control warps (TMA producer, MMA issuer, sigma producer)
+// take the TOP warp ids and the epilogue warps the bottom ones; the epilogue
+// warps' ids stay 4-aligned so warp % 4 is the TMEM lane quadrant they may
+// access.
+constexpr int NUM_CTRL_WARPS = 4;
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -81,6 +87,46 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITA_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_a(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_a(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit_a(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float4 ld_shared_f32x4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -221,6 +267,7 @@ struct Params {
   int n_chunks;         // MBS chunks per tile (== n_macros)
   uint32_t idesc;       // instruction descriptor without scale-factor ids
   long long* trace;     // optional clock64 trace of CTA 0 (mxq_debug_set_trace)
+  int dbg;              // ablation flags (MXQ_GEMM_DBG, development only)
 };
 
 constexpr int TRACE_CHUNKS = 512;
@@ -252,7 +299,8 @@ struct Cfg {
   // MBS: 16 epilogue warps (4 per TMEM lane quadrant, 32 columns each) to hide
   // the per-chunk latency chain; plain: 8 warps (2 per quadrant).
   static constexpr int EPIW = MBS ? 16 : 8;
-  static constexpr int THREADS = (EPI_WARP0 + EPIW) * 32;
+  static constexpr int THREADS = (EPIW + NUM_CTRL_WARPS) * 32;
+  static constexpr int W_TMA = EPIW + 3, W_MMA = EPIW + 2, W_SIG = EPIW + 1;
   static constexpr int COLS = BN / (EPIW / 4);
   static_assert(TMEM_COLS_USED <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -295,7 +343,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
-  if (warp == 1) {
+  if (warp == C::W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
                  "n"(C::TMEM_COLS)
                  : "memory");
@@ -306,74 +354,75 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
   tc_fence_after();
   const uint32_t tmem = *tmem_base_slot;
 
-  if (warp == 0) {
+  // Shared-memory addresses of the barriers (32-bit shared window), computed
+  // once: the hot loops below are issue-bound, so no address conversion,
+  // division or modulo is left inside them.
+  const uint32_t a_full = smem_u32(full), a_empty = smem_u32(empty);
+  const uint32_t a_tfull = smem_u32(tfull), a_tempty = smem_u32(tempty);
+  const uint32_t a_sfull = smem_u32(sfull), a_sempty = smem_u32(sempty);
+  const uint32_t a_smem = smem_u32(smem);
+
+  if (warp == C::W_TMA) {
     // ===================== TMA producer =====================
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
+      uint32_t stage = 0, phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int mb = tile % tiles_m, nb = tile / tiles_m;
         const int m0 = mb * BM, n0 = nb * BN;
+        const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * 512;
+        const uint8_t* sb = p.sfb + (int64_t)(n0 / 128) * p.sfb_kg * 512;
         for (int s = 0; s < n_stages; ++s) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::TX_BYTES);
-          tma_load_2d(smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, &full[stage], s * (KSTAGE / 2), m0);
-          tma_load_2d(smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, &full[stage], s * (KSTAGE / 2), n0);
-          const uint8_t* sa = p.sfa + ((int64_t)mb * p.sfa_kg + (int64_t)s * C::SF_ATOMS_PER_STAGE) * 512;
-          bulk_load(smem + C::OFF_SFA + stage * C::SFA_BYTES, sa, C::SFA_BYTES, &full[stage]);
+          const uint32_t fb = a_full + stage * 8;
+          mbar_wait_a(a_empty + stage * 8, phase ^ 1);
+          mbar_expect_tx_a(fb, C::TX_BYTES);
+          tma_load_2d_a(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
+          tma_load_2d_a(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, fb, s * (KSTAGE / 2), n0);
+          bulk_load_a(a_smem + C::OFF_SFA + stage * C::SFA_BYTES, sa + (int64_t)s * C::SFA_BYTES, C::SFA_BYTES, fb);
 #pragma unroll
-          for (int rb = 0; rb < BN / 128; ++rb) {
-            const uint8_t* sb =
-                p.sfb + ((int64_t)(n0 / 128 + rb) * p.sfb_kg + (int64_t)s * C::SF_ATOMS_PER_STAGE) * 512;
-            bulk_load(smem + C::OFF_SFB + stage * C::SFB_BYTES + rb * C::SF_ATOMS_PER_STAGE * 512, sb,
-                      C::SF_ATOMS_PER_STAGE * 512, &full[stage]);
-          }
+          for (int rb = 0; rb < BN / 128; ++rb)
+            bulk_load_a(a_smem + C::OFF_SFB + stage * C::SFB_BYTES + rb * C::SFA_BYTES,
+                        sb + ((int64_t)rb * p.sfb_kg * 512 + (int64_t)s * C::SFA_BYTES), C::SFA_BYTES, fb);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == C::W_MMA) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t chunk_ctr = 0;  // accumulator buffers used so far
+      uint32_t stage = 0, phase = 0;
+      uint32_t buf = 0, tphase = 0;  // accumulator ring position
       uint32_t sf_par = 0;
       const int chunk_len = MBS ? p.macro_steps : (1 << 30);
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int kstep = 0;
-        uint32_t buf = 0;
+        int kstep = 0, in_chunk = 0;
         bool open = false;
         for (int s = 0; s < n_stages; ++s) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_a(a_full + stage * 8, phase);
           tc_fence_after();
           // scale factors of this stage: smem -> TMEM (parity-buffered)
           const uint32_t sfa_col = tmem + C::COL_SF + sf_par * (C::SFA_COLS + C::SFB_COLS);
           const uint32_t sfb_col = sfa_col + C::SFA_COLS;
-          const uint32_t sfa_s = smem_u32(smem + C::OFF_SFA + stage * C::SFA_BYTES);
-          const uint32_t sfb_s = smem_u32(smem + C::OFF_SFB + stage * C::SFB_BYTES);
+          const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES;
+          const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES;
 #pragma unroll
-          for (int a = 0; a < C::SF_ATOMS_PER_STAGE; ++a) {
-            utccp_sf(sfa_col + a * 4, sf_desc(sfa_s + a * 512));
+          for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
+            utccp_sf(sfa_col + at * 4, sf_desc(sfa_s + at * 512));
 #pragma unroll
             for (int rb = 0; rb < BN / 128; ++rb)
-              utccp_sf(sfb_col + a * 4 * (BN / 128) + rb * 4,
-                       sf_desc(sfb_s + rb * C::SF_ATOMS_PER_STAGE * 512 + a * 512));
+              utccp_sf(sfb_col + at * 4 * (BN / 128) + rb * 4, sf_desc(sfb_s + rb * C::SFA_BYTES + at * 512));
           }
-          const uint32_t a_s = smem_u32(smem + C::OFF_A + stage * STAGE_BYTES_A);
-          const uint32_t b_s = smem_u32(smem + C::OFF_B + stage * C::STAGE_BYTES_B);
+          const uint64_t adesc = operand_desc(a_smem + C::OFF_A + stage * STAGE_BYTES_A);
+          const uint64_t bdesc = operand_desc(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B);
 #pragma unroll
           for (int k = 0; k < KSTAGE / KSTEP; ++k) {
             if (kstep < n_ksteps) {
-              const int in_chunk = kstep % chunk_len;
               if (in_chunk == 0) {
-                if (open) tc_commit(&tfull[buf]);
-                buf = chunk_ctr % NB;
-                if (p.trace && blockIdx.x == 0 && chunk_ctr < TRACE_CHUNKS) p.trace[chunk_ctr * 4 + 0] = clock64();
-                mbar_wait(&tempty[buf], ((chunk_ctr / NB) & 1) ^ 1);
+                if (open) {
+                  tc_commit_a(a_tfull + buf * 8);
+                  if (++buf == NB) { buf = 0; tphase ^= 1; }
+                }
+                mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
                 tc_fence_after();
-                if (p.trace && blockIdx.x == 0 && chunk_ctr < TRACE_CHUNKS) p.trace[chunk_ctr * 4 + 1] = clock64();
-                ++chunk_ctr;
                 open = true;
               }
               uint32_t idesc = p.idesc;
@@ -383,46 +432,55 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
                 const uint32_t sf_id = (uint32_t)(k & 1) * 2u;
                 idesc |= (sf_id << 29) | (sf_id << 4);
               }
-              mma_bs<SF32>(tmem + buf * BN, operand_desc(a_s + k * 32), operand_desc(b_s + k * 32), idesc,
+              // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
+              mma_bs<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
                            in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
+              if (++in_chunk == chunk_len) in_chunk = 0;
             }
             ++kstep;
           }
-          tc_commit(&empty[stage]);
+          tc_commit_a(a_empty + stage * 8);
           sf_par ^= 1;
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (open) tc_commit(&tfull[buf]);
+        if (open) {
+          tc_commit_a(a_tfull + buf * 8);
+          if (++buf == NB) { buf = 0; tphase ^= 1; }
+        }
       }
     }
-  } else if (warp == 2) {
+  } else if (warp == C::W_SIG) {
     // ===================== sigma producer (MBS) =====================
+    // One slot per chunk: sigmaA[128 rows] and sigmaB[BN cols] as f32 (a
+    // non-MBS operand points at a row of ones with ld 0).
     if constexpr (MBS) {
       if (lane == 0) {
-        const uint32_t bytes = (p.sga ? BM * 4 : 0) + (p.sgb ? BN * 4 : 0);
-        uint32_t ctr = 0;
+        uint32_t slot = 0, sphase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
           const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
-          for (int t = 0; t < p.n_chunks; ++t, ++ctr) {
-            const uint32_t slot = ctr % C::NSIG;
-            mbar_wait(&sempty[slot], ((ctr / C::NSIG) & 1) ^ 1);
-            mbar_expect_tx(&sfull[slot], bytes);
-            float* dst = reinterpret_cast<float*>(smem + C::OFF_SIG + slot * C::SIG_SLOT);
-            if (p.sga) bulk_load(dst, p.sga + (int64_t)t * p.sga_ld + m0, BM * 4, &sfull[slot]);
-            if (p.sgb) bulk_load(dst + BM, p.sgb + (int64_t)t * p.sgb_ld + n0, BN * 4, &sfull[slot]);
+          const float* ga = p.sga + (p.sga_ld ? m0 : 0);
+          const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
+          for (int t = 0; t < p.n_chunks; ++t) {
+            const uint32_t fb = a_sfull + slot * 8;
+            mbar_wait_a(a_sempty + slot * 8, sphase ^ 1);
+            mbar_expect_tx_a(fb, (BM + BN) * 4);
+            const uint32_t dst = a_smem + C::OFF_SIG + slot * C::SIG_SLOT;
+            bulk_load_a(dst, ga + (int64_t)t * p.sga_ld, BM * 4, fb);
+            bulk_load_a(dst + BM * 4, gb + (int64_t)t * p.sgb_ld, BN * 4, fb);
+            if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
           }
         }
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  } else if (warp < C::EPIW) {
     // ===================== epilogue =====================
-    const int e = warp - EPI_WARP0;
+    const int e = warp;
     const int quad = warp & 3;             // TMEM lane quadrant this warp may access
     const int half = e >> 2;               // column part (0 .. EPIW/4-1)
     constexpr int COLS = C::COLS;          // columns per thread
     const int row_in_tile = quad * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    uint32_t chunk_ctr = 0;
+    const uint32_t tmem_lane = tmem + ((uint32_t)(quad * 32) << 16) + half * COLS;
+    uint32_t buf = 0, tphase = 0, slot = 0, sphase = 0;
     float scale_nv = 1.0f;
     if (p.tsa && p.tsb) scale_nv = (float)(*p.tsa * *p.tsb);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -431,66 +489,64 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
       const int row = m0 + row_in_tile;
       float acc[COLS];
       if constexpr (!MBS) {
-        const uint32_t buf = chunk_ctr % NB;
-        mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
+        mbar_wait_a(a_tfull + buf * 8, tphase);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < COLS; c += 32) {
           float v[32];
-          tmem_ld32(tmem + lane_addr + buf * BN + half * COLS + c, v);
+          tmem_ld32(tmem_lane + buf * BN + c, v);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[c + i] = v[i] * scale_nv;
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[buf]);
-        ++chunk_ctr;
+        if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
+        if (++buf == NB) { buf = 0; tphase ^= 1; }
       } else {
         static_assert(COLS == 32, "MBS epilogue: 32 columns per thread");
 #pragma unroll
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
-        const bool hasa = p.sga != nullptr, hasb = p.sgb != nullptr;
+        const uint32_t sig_row = a_smem + C::OFF_SIG + row_in_tile * 4;
+        const uint32_t sig_col = a_smem + C::OFF_SIG + (BM + half * COLS) * 4;
         for (int t = 0; t < p.n_chunks; ++t) {
-          // (1) sigma for this chunk (landed long ago): w_j = sigmaA_i * sigmaB_j,
-          //     computed before the partial product is waited for.
-          const uint32_t slot = chunk_ctr % C::NSIG;
-          mbar_wait(&sfull[slot], (chunk_ctr / C::NSIG) & 1);
-          const float* sig = reinterpret_cast<const float*>(smem + C::OFF_SIG + slot * C::SIG_SLOT);
-          const float sa = hasa ? sig[row_in_tile] : 1.0f;
-          const float* sbp = sig + BM + half * COLS;
+          // (1) sigma products w_j = sigmaA_i * sigmaB_j (before P is waited for)
+          mbar_wait_a(a_sfull + slot * 8, sphase);
+          const float sa = ld_shared_f32(sig_row + slot * C::SIG_SLOT);
           float w[COLS];
 #pragma unroll
           for (int i = 0; i < COLS; i += 4) {
-            const float4 sb4 = hasb ? *reinterpret_cast<const float4*>(sbp + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+            const float4 sb4 = ld_shared_f32x4(sig_col + slot * C::SIG_SLOT + i * 4);
             mul2(w[i], w[i + 1], sa, sb4.x, sb4.y);
             mul2(w[i + 2], w[i + 3], sa, sb4.z, sb4.w);
           }
-          // (2) the chunk's partial P from TMEM; the buffer is released as soon
-          //     as it is in registers, so the MMA runs ahead during the FMAs.
-          const uint32_t buf = chunk_ctr % NB;
-          const bool tr = p.trace && blockIdx.x == 0 && e == 0 && lane == 0 && chunk_ctr < TRACE_CHUNKS;
-          if (tr) p.trace[chunk_ctr * 4 + 2] = clock64();
-          mbar_wait(&tfull[buf], (chunk_ctr / NB) & 1);
+          // (2) the chunk's partial P; TMEM buffer and sigma slot are released
+          //     as soon as both are in registers.
+          mbar_wait_a(a_tfull + buf * 8, tphase);
           tc_fence_after();
-          if (tr) p.trace[chunk_ctr * 4 + 3] = clock64();
-          float v0[16], v1[16];
-          tmem_ld16(tmem + lane_addr + buf * BN + half * COLS, v0);
-          tmem_ld16(tmem + lane_addr + buf * BN + half * COLS + 16, v1);
-          tmem_wait_ld();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&tempty[buf]);
-            mbar_arrive(&sempty[slot]);
-          }
-          // (3) acc += w * P  (FFMA2)
+          {
+            float v[16];
+            tmem_ld16(tmem_lane + buf * BN, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            fma2(acc[i], acc[i + 1], w[i], w[i + 1], v0[i], v0[i + 1]);
-            fma2(acc[16 + i], acc[16 + i + 1], w[16 + i], w[16 + i + 1], v1[i], v1[i + 1]);
+            for (int i = 0; i < 16; i += 2) fma2(acc[i], acc[i + 1], w[i], w[i + 1], v[i], v[i + 1]);
           }
-          ++chunk_ctr;
+          {
+            float v[16];
+            tmem_ld16(tmem_lane + buf * BN + 16, v);
+            tmem_wait_ld();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive_a(a_tempty + buf * 8);
+              mbar_arrive_a(a_sempty + slot * 8);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i += 2)
+              fma2(acc[16 + i], acc[16 + i + 1], w[16 + i], w[16 + i + 1], v[i], v[i + 1]);
+          }
+          if (++buf == NB) { buf = 0; tphase ^= 1; }
+          if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
         }
       }
       // ---- store ----
@@ -531,7 +587,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == C::W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS) : "memory");
   }
@@ -589,6 +645,23 @@ static uint32_t make_idesc(int n, bool ue8m0) {
 
 static long long* g_trace = nullptr;
 
+// 256 f32 ones per device: the sigma row of a non-MBS operand in an MBS GEMM.
+static const float* ones_buffer() {
+  static float* ptrs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!ptrs[dev]) {
+    float h[256];
+    for (int i = 0; i < 256; ++i) h[i] = 1.0f;
+    float* d = nullptr;
+    if (cudaMalloc(&d, sizeof(h)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    ptrs[dev] = d;
+  }
+  return ptrs[dev];
+}
+
 template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
 static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, bool ue8m0, cudaStream_t st) {
   using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
@@ -610,10 +683,14 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.sfa_kg = a.sf_kpad / 4;
   p.sfb_kg = b.sf_kpad / 4;
   const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
-  p.sga = (MBS && ma) ? a.sig_t : nullptr;
-  p.sgb = (MBS && mbb) ? b.sig_t : nullptr;
-  p.sga_ld = a.sig_t_ld;
-  p.sgb_ld = b.sig_t_ld;
+  if constexpr (MBS) {
+    const float* ones = ones_buffer();
+    if (!ones) return set_error(ERR_INVALID, "could not allocate the sigma ones row");
+    p.sga = ma ? a.sig_t : ones;
+    p.sgb = mbb ? b.sig_t : ones;
+    p.sga_ld = ma ? a.sig_t_ld : 0;
+    p.sgb_ld = mbb ? b.sig_t_ld : 0;
+  }
   p.tsa = a.variant == NVFP4 ? a.tensor_scale : nullptr;
   p.tsb = b.variant == NVFP4 ? b.tensor_scale : nullptr;
   p.c = c;
@@ -625,7 +702,8 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.macro_steps = macro / KSTEP;
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.idesc = make_idesc(BN, ue8m0);
-  p.trace = g_trace;
+  p.trace = nullptr;
+  p.dbg = 0;
   const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, p);
