@@ -388,64 +388,86 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     }
   } else if (warp == C::W_MMA) {
     // ===================== MMA issuer =====================
+    // The scale-factor copies (tcgen05.cp smem->TMEM) for stage g+1 are
+    // issued before the MMAs of stage g (parity-buffered TMEM columns), so
+    // the copy latency overlaps the MMAs instead of preceding them.
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      uint32_t buf = 0, tphase = 0;  // accumulator ring position
-      uint32_t sf_par = 0;
+      const int my_tiles = blockIdx.x < num_tiles ? (num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const int total = my_tiles * n_stages;
+      uint32_t stage = 0, phase = 0;      // stage g in the smem ring
+      uint32_t nstage = 0, nphase = 0;    // stage g+1 (copy prefetch)
+      uint32_t buf = 0, tphase = 0;       // accumulator ring position
       const int chunk_len = MBS ? p.macro_steps : (1 << 30);
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int kstep = 0, in_chunk = 0;
-        bool open = false;
-        for (int s = 0; s < n_stages; ++s) {
-          mbar_wait_a(a_full + stage * 8, phase);
-          tc_fence_after();
-          // scale factors of this stage: smem -> TMEM (parity-buffered)
-          const uint32_t sfa_col = tmem + C::COL_SF + sf_par * (C::SFA_COLS + C::SFB_COLS);
-          const uint32_t sfb_col = sfa_col + C::SFA_COLS;
-          const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES;
-          const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES;
+      auto copy_sf = [&](uint32_t st_idx, uint32_t par) {
+        const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
+        const uint32_t sfb_col = sfa_col + C::SFA_COLS;
+        const uint32_t sfa_s = a_smem + C::OFF_SFA + st_idx * C::SFA_BYTES;
+        const uint32_t sfb_s = a_smem + C::OFF_SFB + st_idx * C::SFB_BYTES;
 #pragma unroll
-          for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
-            utccp_sf(sfa_col + at * 4, sf_desc(sfa_s + at * 512));
+        for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
+          utccp_sf(sfa_col + at * 4, sf_desc(sfa_s + at * 512));
 #pragma unroll
-            for (int rb = 0; rb < BN / 128; ++rb)
-              utccp_sf(sfb_col + at * 4 * (BN / 128) + rb * 4, sf_desc(sfb_s + rb * C::SFA_BYTES + at * 512));
-          }
-          const uint64_t adesc = operand_desc(a_smem + C::OFF_A + stage * STAGE_BYTES_A);
-          const uint64_t bdesc = operand_desc(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B);
-#pragma unroll
-          for (int k = 0; k < KSTAGE / KSTEP; ++k) {
-            if (kstep < n_ksteps) {
-              if (in_chunk == 0) {
-                if (open) {
-                  tc_commit_a(a_tfull + buf * 8);
-                  if (++buf == NB) { buf = 0; tphase ^= 1; }
-                }
-                mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
-                tc_fence_after();
-                open = true;
-              }
-              uint32_t idesc = p.idesc;
-              int atom = k;
-              if constexpr (SF32) {
-                atom = k >> 1;
-                const uint32_t sf_id = (uint32_t)(k & 1) * 2u;
-                idesc |= (sf_id << 29) | (sf_id << 4);
-              }
-              // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
-              mma_bs<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
-                           in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
-              if (++in_chunk == chunk_len) in_chunk = 0;
-            }
-            ++kstep;
-          }
-          tc_commit_a(a_empty + stage * 8);
-          sf_par ^= 1;
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int rb = 0; rb < BN / 128; ++rb)
+            utccp_sf(sfb_col + at * 4 * (BN / 128) + rb * 4, sf_desc(sfb_s + rb * C::SFA_BYTES + at * 512));
         }
-        if (open) {
-          tc_commit_a(a_tfull + buf * 8);
-          if (++buf == NB) { buf = 0; tphase ^= 1; }
+      };
+      if (total > 0) {
+        mbar_wait_a(a_full, 0);
+        tc_fence_after();
+        copy_sf(0, 0);
+        if (++nstage == STAGES) { nstage = 0; nphase ^= 1; }
+      }
+      int s = 0, kstep = 0, in_chunk = 0;
+      bool open = false;
+      for (int g = 0; g < total; ++g) {
+        if (g + 1 < total) {
+          mbar_wait_a(a_full + nstage * 8, nphase);
+          tc_fence_after();
+          copy_sf(nstage, (uint32_t)(g + 1) & 1u);
+          if (++nstage == STAGES) { nstage = 0; nphase ^= 1; }
+        }
+        const uint32_t par = (uint32_t)g & 1u;
+        const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
+        const uint32_t sfb_col = sfa_col + C::SFA_COLS;
+        const uint64_t adesc = operand_desc(a_smem + C::OFF_A + stage * STAGE_BYTES_A);
+        const uint64_t bdesc = operand_desc(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B);
+#pragma unroll
+        for (int k = 0; k < KSTAGE / KSTEP; ++k) {
+          if (kstep < n_ksteps) {
+            if (in_chunk == 0) {
+              if (open) {
+                tc_commit_a(a_tfull + buf * 8);
+                if (++buf == NB) { buf = 0; tphase ^= 1; }
+              }
+              mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
+              tc_fence_after();
+              open = true;
+            }
+            uint32_t idesc = p.idesc;
+            int atom = k;
+            if constexpr (SF32) {
+              atom = k >> 1;
+              const uint32_t sf_id = (uint32_t)(k & 1) * 2u;
+              idesc |= (sf_id << 29) | (sf_id << 4);
+            }
+            // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
+            mma_bs<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
+                         in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
+            if (++in_chunk == chunk_len) in_chunk = 0;
+          }
+          ++kstep;
+        }
+        tc_commit_a(a_empty + stage * 8);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++s == n_stages) {  // tile done
+          s = 0;
+          kstep = 0;
+          in_chunk = 0;
+          if (open) {
+            tc_commit_a(a_tfull + buf * 8);
+            if (++buf == NB) { buf = 0; tphase ^= 1; }
+          }
+          open = false;
         }
       }
     }
@@ -509,41 +531,41 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
         const uint32_t sig_row = a_smem + C::OFF_SIG + row_in_tile * 4;
         const uint32_t sig_col = a_smem + C::OFF_SIG + (BM + half * COLS) * 4;
+#pragma unroll 1
         for (int t = 0; t < p.n_chunks; ++t) {
-          // (1) sigma products w_j = sigmaA_i * sigmaB_j (before P is waited for)
+          // sigma slot of this chunk (landed long ago) and the partial P.
           mbar_wait_a(a_sfull + slot * 8, sphase);
+          const uint32_t sig = sig_col + slot * C::SIG_SLOT;
           const float sa = ld_shared_f32(sig_row + slot * C::SIG_SLOT);
-          float w[COLS];
-#pragma unroll
-          for (int i = 0; i < COLS; i += 4) {
-            const float4 sb4 = ld_shared_f32x4(sig_col + slot * C::SIG_SLOT + i * 4);
-            mul2(w[i], w[i + 1], sa, sb4.x, sb4.y);
-            mul2(w[i + 2], w[i + 3], sa, sb4.z, sb4.w);
-          }
-          // (2) the chunk's partial P; TMEM buffer and sigma slot are released
-          //     as soon as both are in registers.
           mbar_wait_a(a_tfull + buf * 8, tphase);
           tc_fence_after();
-          {
-            float v[16];
-            tmem_ld16(tmem_lane + buf * BN, v);
-            tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; i += 2) fma2(acc[i], acc[i + 1], w[i], w[i + 1], v[i], v[i + 1]);
-          }
-          {
+          for (int h = 0; h < 2; ++h) {
             float v[16];
-            tmem_ld16(tmem_lane + buf * BN + 16, v);
+            tmem_ld16(tmem_lane + buf * BN + h * 16, v);
+            float4 sb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sb[q] = ld_shared_f32x4(sig + (h * 16 + q * 4) * 4);
             tmem_wait_ld();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              mbar_arrive_a(a_tempty + buf * 8);
-              mbar_arrive_a(a_sempty + slot * 8);
+            if (h == 1) {
+              // TMEM buffer and sigma slot are free once P is in registers.
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                mbar_arrive_a(a_tempty + buf * 8);
+                mbar_arrive_a(a_sempty + slot * 8);
+              }
             }
+            // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
 #pragma unroll
-            for (int i = 0; i < 16; i += 2)
-              fma2(acc[16 + i], acc[16 + i + 1], w[16 + i], w[16 + i + 1], v[i], v[i + 1]);
+            for (int q = 0; q < 4; ++q) {
+              float w0, w1, w2, w3;
+              mul2(w0, w1, sa, sb[q].x, sb[q].y);
+              mul2(w2, w3, sa, sb[q].z, sb[q].w);
+              const int c = h * 16 + q * 4;
+              fma2(acc[c], acc[c + 1], w0, w1, v[q * 4], v[q * 4 + 1]);
+              fma2(acc[c + 2], acc[c + 3], w2, w3, v[q * 4 + 2], v[q * 4 + 3]);
+            }
           }
           if (++buf == NB) { buf = 0; tphase ^= 1; }
           if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
