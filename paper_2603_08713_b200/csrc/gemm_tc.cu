@@ -397,7 +397,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
       uint32_t stage = 0, phase = 0;      // stage g in the smem ring
       uint32_t nstage = 0, nphase = 0;    // stage g+1 (copy prefetch)
       uint32_t buf = 0, tphase = 0;       // accumulator ring position
-      const int chunk_len = MBS ? p.macro_steps : (1 << 30);
+      const int dbgm = p.dbg & 3;   // 1: switch D per chunk, no handoff; 2: no switch, no handoff
+      const int chunk_len = (MBS && dbgm != 2) ? p.macro_steps : (1 << 30);
+      int dchunk = 0;
       auto copy_sf = [&](uint32_t st_idx, uint32_t par) {
         const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
         const uint32_t sfb_col = sfa_col + C::SFA_COLS;
@@ -435,6 +437,16 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
         for (int k = 0; k < KSTAGE / KSTEP; ++k) {
           if (kstep < n_ksteps) {
             if (in_chunk == 0) {
+              if (dbgm) {
+                if (!open) {
+                  mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
+                  tc_fence_after();
+                  open = true;
+                  dchunk = 0;
+                } else {
+                  dchunk ^= 1;
+                }
+              } else {
               if (open) {
                 tc_commit_a(a_tfull + buf * 8);
                 if (++buf == NB) { buf = 0; tphase ^= 1; }
@@ -442,6 +454,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
               mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
               tc_fence_after();
               open = true;
+              }
             }
             uint32_t idesc = p.idesc;
             int atom = k;
@@ -451,7 +464,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
               idesc |= (sf_id << 29) | (sf_id << 4);
             }
             // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
-            mma_bs<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
+            mma_bs<SF32>(tmem + buf * BN + (dbgm == 1 ? dchunk * BN : 0), adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
                          in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
             if (++in_chunk == chunk_len) in_chunk = 0;
           }
@@ -476,7 +489,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     // One slot per chunk: sigmaA[128 rows] and sigmaB[BN cols] as f32 (a
     // non-MBS operand points at a row of ones with ld 0).
     if constexpr (MBS) {
-      if (lane == 0) {
+      if (lane == 0 && !(p.dbg & 3)) {
         uint32_t slot = 0, sphase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
           const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
@@ -510,7 +523,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
       const int m0 = mb * BM, n0 = nb * BN;
       const int row = m0 + row_in_tile;
       float acc[COLS];
-      if constexpr (!MBS) {
+      if (!MBS || (p.dbg & 3)) {
         mbar_wait_a(a_tfull + buf * 8, tphase);
         tc_fence_after();
 #pragma unroll
@@ -525,7 +538,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
         __syncwarp();
         if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
         if (++buf == NB) { buf = 0; tphase ^= 1; }
-      } else {
+      } else if constexpr (MBS) {
         static_assert(COLS == 32, "MBS epilogue: 32 columns per thread");
 #pragma unroll
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
@@ -667,6 +680,18 @@ static uint32_t make_idesc(int n, bool ue8m0) {
 
 static long long* g_trace = nullptr;
 
+// Development experiments (MXQ_GEMM_DBG, read once): 1 = switch the MBS
+// accumulator per chunk without the epilogue hand-off, 2 = no switch either.
+// Both change numerics on purpose; 0 (unset) is the product path.
+static int debug_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* d = getenv("MXQ_GEMM_DBG");
+    v = d ? atoi(d) : 0;
+  }
+  return v;
+}
+
 // 256 f32 ones per device: the sigma row of a non-MBS operand in an MBS GEMM.
 static const float* ones_buffer() {
   static float* ptrs[64] = {nullptr};
@@ -725,7 +750,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.idesc = make_idesc(BN, ue8m0);
   p.trace = nullptr;
-  p.dbg = 0;
+  p.dbg = debug_flags();
   const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
   int grid = tiles < num_sms() ? tiles : num_sms();
   kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, p);

@@ -1,7 +1,7 @@
 #!/bin/bash
-# MBS GEMM ablations (timing only; flags break numerics on purpose)
+# GEMM timing experiments (dev only; modes 1/2 change numerics on purpose)
 export PYTHONPATH=$PWD
-for f in 0 512 1024 1536 1540; do
+for f in ${FLAGS:-0 1 2}; do
   echo "== MXQ_GEMM_DBG=$f"
   MXQ_GEMM_DBG=$f timeout 60 python - <<'PY'
 import torch, paper_2603_08713_b200 as M
@@ -20,6 +20,6 @@ for n in (4096, 8192):
         for _ in range(10): M.matmul_quantized(aq, wq, out=out, out_dtype=torch.bfloat16)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        print(f"  {va.value}x{vw.value} {n}: {ms*1e3:.1f} us {2*n**3/ms/1e9:.0f} TFLOP/s")
+        print(f"  {va.value}x{vw.value} {n}: {ms*1e3:.1f} us {2*n**3/ms/1e9:.0f} TFLOP/s", flush=True)
 PY
 done
