@@ -1,5 +1,6 @@
 """Quick device timing of the tcgen05 GEMM variants (development aid)."""
-import sys
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 import paper_2603_08713_b200 as M
