@@ -115,6 +115,26 @@ __device__ __forceinline__ void bulk_load_a(uint32_t dst, const void* src, uint3
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+      : "memory");
+}
+// MMA completion arrives on the barrier at the same smem offset in every CTA
+// of `mask` (each CTA's stage may be overwritten by a peer's multicast only
+// after every consumer in the cluster is done with it).
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tc_commit_a(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -272,7 +292,7 @@ struct Params {
 
 constexpr int TRACE_CHUNKS = 512;
 
-template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
+template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
 struct Cfg {
   static constexpr int STAGE_BYTES_B = BN * KSTAGE / 2;
   static constexpr int SF_ATOMS_PER_STAGE = SF32 ? 2 : 4;  // 512-B atoms per 128 rows per stage
@@ -306,10 +326,10 @@ struct Cfg {
   static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
-__global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THREADS, 1)
+template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
+__global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
-  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
+  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -321,15 +341,22 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sempty + C::NSIG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Work units: a cluster of CL CTAs takes CL consecutive 128-row blocks of
+  // one BN-column block; the CTAs of a cluster load half of the shared B tile
+  // each and multicast it (halving the L2->SMEM operand traffic for B).
   const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
-  const int num_tiles = tiles_m * tiles_n;
+  const int groups_m = (tiles_m + CL - 1) / CL;
+  const int num_units = groups_m * tiles_n;
+  const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
+  uint32_t crank = 0;
+  if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   const int n_stages = (p.K + KSTAGE - 1) / KSTAGE;
   const int n_ksteps = (p.K + KSTEP - 1) / KSTEP;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
@@ -351,6 +378,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync();  // peers' multicasts must find initialised barriers
   tc_fence_after();
   const uint32_t tmem = *tmem_base_slot;
 
@@ -366,8 +394,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     // ===================== TMA producer =====================
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % tiles_m, nb = tile / tiles_m;
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
+        const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
         const int m0 = mb * BM, n0 = nb * BN;
         const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * 512;
         const uint8_t* sb = p.sfb + (int64_t)(n0 / 128) * p.sfb_kg * 512;
@@ -376,7 +404,12 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
           mbar_wait_a(a_empty + stage * 8, phase ^ 1);
           mbar_expect_tx_a(fb, C::TX_BYTES);
           tma_load_2d_a(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
-          tma_load_2d_a(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, fb, s * (KSTAGE / 2), n0);
+          if constexpr (CL == 1) {
+            tma_load_2d_a(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, fb, s * (KSTAGE / 2), n0);
+          } else {
+            tma_load_2d_mc(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B + crank * (BN / CL) * (KSTAGE / 2), &tmB, fb,
+                           s * (KSTAGE / 2), n0 + (int)crank * (BN / CL), (uint16_t)((1u << CL) - 1));
+          }
           bulk_load_a(a_smem + C::OFF_SFA + stage * C::SFA_BYTES, sa + (int64_t)s * C::SFA_BYTES, C::SFA_BYTES, fb);
 #pragma unroll
           for (int rb = 0; rb < BN / 128; ++rb)
@@ -392,7 +425,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     // issued before the MMAs of stage g (parity-buffered TMEM columns), so
     // the copy latency overlaps the MMAs instead of preceding them.
     if (lane == 0) {
-      const int my_tiles = blockIdx.x < num_tiles ? (num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+      const int my_tiles = unit0 < num_units ? (num_units - 1 - unit0) / unit_step + 1 : 0;
       const int total = my_tiles * n_stages;
       uint32_t stage = 0, phase = 0;      // stage g in the smem ring
       uint32_t nstage = 0, nphase = 0;    // stage g+1 (copy prefetch)
@@ -470,7 +503,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
           }
           ++kstep;
         }
-        tc_commit_a(a_empty + stage * 8);
+        if constexpr (CL == 1) tc_commit_a(a_empty + stage * 8);
+        else tc_commit_mc(a_empty + stage * 8, (uint16_t)((1u << CL) - 1));
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++s == n_stages) {  // tile done
           s = 0;
@@ -491,8 +525,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     if constexpr (MBS) {
       if (lane == 0 && !(p.dbg & 3)) {
         uint32_t slot = 0, sphase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-          const int m0 = (tile % tiles_m) * BM, n0 = (tile / tiles_m) * BN;
+        for (int unit = unit0; unit < num_units; unit += unit_step) {
+          const int m0 = ((unit % groups_m) * CL + (int)crank) * BM, n0 = (unit / groups_m) * BN;
           const float* ga = p.sga + (p.sga_ld ? m0 : 0);
           const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
           for (int t = 0; t < p.n_chunks; ++t) {
@@ -518,8 +552,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
     uint32_t buf = 0, tphase = 0, slot = 0, sphase = 0;
     float scale_nv = 1.0f;
     if (p.tsa && p.tsb) scale_nv = (float)(*p.tsa * *p.tsb);
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int mb = tile % tiles_m, nb = tile / tiles_m;
+    for (int unit = unit0; unit < num_units; unit += unit_step) {
+      const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
       const int m0 = mb * BM, n0 = nb * BN;
       const int row = m0 + row_in_tile;
       float acc[COLS];
@@ -622,6 +656,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>::THRE
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) cluster_sync();
   if (warp == C::W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS) : "memory");
@@ -709,10 +744,10 @@ static const float* ones_buffer() {
   return ptrs[dev];
 }
 
-template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16>
+template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
 static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, bool ue8m0, cudaStream_t st) {
-  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
-  auto kern = k_gemm_tc<BN, STAGES, NB, SF32, MBS, OUT_BF16>;
+  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
+  auto kern = k_gemm_tc<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -722,7 +757,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   CUtensorMap ta, tb;
   int rc = make_code_map(&ta, a.codes, a.rows, a.cols / 2, a.codes_ld, BM);
   if (rc) return rc;
-  rc = make_code_map(&tb, b.codes, b.rows, b.cols / 2, b.codes_ld, BN);
+  rc = make_code_map(&tb, b.codes, b.rows, b.cols / 2, b.codes_ld, BN / CL);
   if (rc) return rc;
   Params p{};
   p.sfa = a.scales_mma;
@@ -751,9 +786,23 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.idesc = make_idesc(BN, ue8m0);
   p.trace = nullptr;
   p.dbg = debug_flags();
-  const int tiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN);
-  int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, C::THREADS, C::SMEM, st>>>(ta, tb, p);
+  const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
+  int clusters = num_sms() / CL;
+  if (units < clusters) clusters = units;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CL);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  if (e != cudaSuccess) return set_cuda_error(e);
   return check_launch();
 }
 
@@ -777,16 +826,16 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
     const int macro = ma ? a.macro_size : b.macro_size;
     if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
     if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
-    if (c_dtype == MXQ_BF16) return launch_variant<128, 5, 3, false, true, true>(a, b, c, ldc, true, st);
-    return launch_variant<128, 5, 3, false, true, false>(a, b, c, ldc, true, st);
+    if (c_dtype == MXQ_BF16) return launch_variant<128, 5, 3, false, true, true, 2>(a, b, c, ldc, true, st);
+    return launch_variant<128, 5, 3, false, true, false, 2>(a, b, c, ldc, true, st);
   }
   if (sf32) {
-    if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, true, false, true>(a, b, c, ldc, true, st);
-    return launch_variant<256, 4, 1, true, false, false>(a, b, c, ldc, true, st);
+    if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, true, false, true, 2>(a, b, c, ldc, true, st);
+    return launch_variant<256, 4, 1, true, false, false, 2>(a, b, c, ldc, true, st);
   }
   const bool ue8m0 = !nva;
-  if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, false, false, true>(a, b, c, ldc, ue8m0, st);
-  return launch_variant<256, 4, 1, false, false, false>(a, b, c, ldc, ue8m0, st);
+  if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, false, false, true, 2>(a, b, c, ldc, ue8m0, st);
+  return launch_variant<256, 4, 1, false, false, false, 2>(a, b, c, ldc, ue8m0, st);
 }
 
 }  // namespace mxq
