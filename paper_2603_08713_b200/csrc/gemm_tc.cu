@@ -42,7 +42,8 @@ constexpr int STAGE_BYTES_A = BM * KSTAGE / 2;  // 16 KB
 // take the TOP warp ids and the epilogue warps the bottom ones; the epilogue
 // warps' ids stay 4-aligned so warp % 4 is the TMEM lane quadrant they may
 // access.
-constexpr int NUM_CTRL_WARPS = 4;
+constexpr int NUM_CTRL_WARPS = 4;   // TMA producer, MMA issuer, sigma producer, spare
+constexpr int NUM_SFW_WARPS = 4;    // scale-factor writers (one per TMEM lane quadrant)
 
 // ---------------------------------------------------------------------------
 // PTX wrappers
@@ -138,6 +139,37 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void tc_commit_a(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ uint4 ld_shared_u32x4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[N]) {
+  static_assert(N == 8 || N == 16 || N == 32, "tmem_st width");
+  if constexpr (N == 8) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+  } else if constexpr (N == 16) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+  } else {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+        "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -292,6 +324,42 @@ struct Params {
 
 constexpr int TRACE_CHUNKS = 512;
 
+// Store 32 consecutive output columns of one row (f32 or bf16), masked to
+// the M x N bounds; 16-byte vector stores when the run is in bounds.
+template <bool OUT_BF16>
+__device__ __forceinline__ void store_row32(const Params& p, int row, int col0, const float (&v)[32]) {
+  if (row >= p.M) return;
+  if constexpr (OUT_BF16) {
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
+    if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        uint4 w;
+        w.x = pack_bf16x2(v[c + 0], v[c + 1]);
+        w.y = pack_bf16x2(v[c + 2], v[c + 3]);
+        w.z = pack_bf16x2(v[c + 4], v[c + 5]);
+        w.w = pack_bf16x2(v[c + 6], v[c + 7]);
+        *reinterpret_cast<uint4*>(out + c) = w;
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (col0 + c < p.N) out[c] = __float2bfloat16_rn(v[c]);
+    }
+  } else {
+    float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col0;
+    if (col0 + 32 <= p.N && (p.ldc % 4) == 0) {
+#pragma unroll
+      for (int c = 0; c < 32; c += 4)
+        *reinterpret_cast<float4*>(out + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (col0 + c < p.N) out[c] = v[c];
+    }
+  }
+}
+
 template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
 struct Cfg {
   static constexpr int STAGE_BYTES_B = BN * KSTAGE / 2;
@@ -307,7 +375,7 @@ struct Cfg {
   static constexpr int SIG_SLOT = (BM + BN) * 4;
   static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
   static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + 4;  // + sf_ready[2], sf_free[2]
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
   static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
   // TMEM columns: NB accumulators of BN columns, then 2 parity sets of SF.
@@ -316,11 +384,12 @@ struct Cfg {
   static constexpr int COL_SF = NB * BN;
   static constexpr int TMEM_COLS_USED = COL_SF + 2 * (SFA_COLS + SFB_COLS);
   static constexpr int TMEM_COLS = 512;
-  // MBS: 16 epilogue warps (4 per TMEM lane quadrant, 32 columns each) to hide
-  // the per-chunk latency chain; plain: 8 warps (2 per quadrant).
-  static constexpr int EPIW = MBS ? 16 : 8;
-  static constexpr int THREADS = (EPIW + NUM_CTRL_WARPS) * 32;
-  static constexpr int W_TMA = EPIW + 3, W_MMA = EPIW + 2, W_SIG = EPIW + 1;
+  // 8 epilogue warps: 2 per TMEM lane quadrant, BN/2 columns each.
+  static constexpr int EPIW = 8;
+  static constexpr int THREADS = (EPIW + NUM_SFW_WARPS + NUM_CTRL_WARPS) * 32;
+  static constexpr int W_SFW = EPIW;  // first SF-writer warp (warpgroup aligned)
+  static constexpr int W_TMA = EPIW + 7, W_MMA = EPIW + 6, W_SIG = EPIW + 5;
+
   static constexpr int COLS = BN / (EPIW / 4);
   static_assert(TMEM_COLS_USED <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -338,7 +407,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
   uint64_t* tempty = tfull + NB;
   uint64_t* sfull = tempty + NB;
   uint64_t* sempty = sfull + C::NSIG;
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sempty + C::NSIG);
+  uint64_t* sf_ready = sempty + C::NSIG;  // [2] SF parity buffer written (4 SF-writer warps)
+  uint64_t* sf_free = sf_ready + 2;        // [2] SF parity buffer consumed (MMA commit)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sf_free + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Work units: a cluster of CL CTAs takes CL consecutive 128-row blocks of
@@ -366,6 +437,10 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       mbar_init(&sfull[b], 1);
       mbar_init(&sempty[b], C::EPIW);
     }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sf_ready[b], NUM_SFW_WARPS);
+      mbar_init(&sf_free[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -388,7 +463,10 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
   const uint32_t a_full = smem_u32(full), a_empty = smem_u32(empty);
   const uint32_t a_tfull = smem_u32(tfull), a_tempty = smem_u32(tempty);
   const uint32_t a_sfull = smem_u32(sfull), a_sempty = smem_u32(sempty);
+  const uint32_t a_sf_ready = smem_u32(sf_ready), a_sf_free = smem_u32(sf_free);
   const uint32_t a_smem = smem_u32(smem);
+
+  const int my_units = unit0 < num_units ? (num_units - 1 - unit0) / unit_step + 1 : 0;
 
   if (warp == C::W_TMA) {
     // ===================== TMA producer =====================
@@ -421,47 +499,20 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     }
   } else if (warp == C::W_MMA) {
     // ===================== MMA issuer =====================
-    // The scale-factor copies (tcgen05.cp smem->TMEM) for stage g+1 are
-    // issued before the MMAs of stage g (parity-buffered TMEM columns), so
-    // the copy latency overlaps the MMAs instead of preceding them.
+    // Scale factors reach TMEM through the SF-writer warps (tcgen05.st), not
+    // tcgen05.cp: the tensor pipe only runs MMAs.
     if (lane == 0) {
-      const int my_tiles = unit0 < num_units ? (num_units - 1 - unit0) / unit_step + 1 : 0;
-      const int total = my_tiles * n_stages;
+      const int total = my_units * n_stages;
       uint32_t stage = 0, phase = 0;      // stage g in the smem ring
-      uint32_t nstage = 0, nphase = 0;    // stage g+1 (copy prefetch)
       uint32_t buf = 0, tphase = 0;       // accumulator ring position
-      const int dbgm = p.dbg & 3;   // 1: switch D per chunk, no handoff; 2: no switch, no handoff
-      const int chunk_len = (MBS && dbgm != 2) ? p.macro_steps : (1 << 30);
-      int dchunk = 0;
-      auto copy_sf = [&](uint32_t st_idx, uint32_t par) {
-        const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
-        const uint32_t sfb_col = sfa_col + C::SFA_COLS;
-        const uint32_t sfa_s = a_smem + C::OFF_SFA + st_idx * C::SFA_BYTES;
-        const uint32_t sfb_s = a_smem + C::OFF_SFB + st_idx * C::SFB_BYTES;
-#pragma unroll
-        for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
-          utccp_sf(sfa_col + at * 4, sf_desc(sfa_s + at * 512));
-#pragma unroll
-          for (int rb = 0; rb < BN / 128; ++rb)
-            utccp_sf(sfb_col + at * 4 * (BN / 128) + rb * 4, sf_desc(sfb_s + rb * C::SFA_BYTES + at * 512));
-        }
-      };
-      if (total > 0) {
-        mbar_wait_a(a_full, 0);
-        tc_fence_after();
-        copy_sf(0, 0);
-        if (++nstage == STAGES) { nstage = 0; nphase ^= 1; }
-      }
+      const int chunk_len = MBS ? p.macro_steps : (1 << 30);
       int s = 0, kstep = 0, in_chunk = 0;
       bool open = false;
       for (int g = 0; g < total; ++g) {
-        if (g + 1 < total) {
-          mbar_wait_a(a_full + nstage * 8, nphase);
-          tc_fence_after();
-          copy_sf(nstage, (uint32_t)(g + 1) & 1u);
-          if (++nstage == STAGES) { nstage = 0; nphase ^= 1; }
-        }
         const uint32_t par = (uint32_t)g & 1u;
+        mbar_wait_a(a_full + stage * 8, phase);
+        mbar_wait_a(a_sf_ready + par * 8, ((uint32_t)g >> 1) & 1u);
+        tc_fence_after();
         const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
         const uint32_t sfb_col = sfa_col + C::SFA_COLS;
         const uint64_t adesc = operand_desc(a_smem + C::OFF_A + stage * STAGE_BYTES_A);
@@ -470,16 +521,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         for (int k = 0; k < KSTAGE / KSTEP; ++k) {
           if (kstep < n_ksteps) {
             if (in_chunk == 0) {
-              if (dbgm) {
-                if (!open) {
-                  mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
-                  tc_fence_after();
-                  open = true;
-                  dchunk = 0;
-                } else {
-                  dchunk ^= 1;
-                }
-              } else {
               if (open) {
                 tc_commit_a(a_tfull + buf * 8);
                 if (++buf == NB) { buf = 0; tphase ^= 1; }
@@ -487,7 +528,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
               mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
               tc_fence_after();
               open = true;
-              }
             }
             uint32_t idesc = p.idesc;
             int atom = k;
@@ -497,7 +537,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
               idesc |= (sf_id << 29) | (sf_id << 4);
             }
             // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
-            mma_bs<SF32>(tmem + buf * BN + (dbgm == 1 ? dchunk * BN : 0), adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
+            mma_bs<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
                          in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
             if (++in_chunk == chunk_len) in_chunk = 0;
           }
@@ -505,6 +545,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         }
         if constexpr (CL == 1) tc_commit_a(a_empty + stage * 8);
         else tc_commit_mc(a_empty + stage * 8, (uint16_t)((1u << CL) - 1));
+        tc_commit_a(a_sf_free + par * 8);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++s == n_stages) {  // tile done
           s = 0;
@@ -517,6 +558,52 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           open = false;
         }
       }
+    }
+  } else if (warp >= C::W_SFW && warp < C::W_SFW + NUM_SFW_WARPS) {
+    // ===================== scale-factor writers =====================
+    // Warp q writes TMEM lanes 32q..32q+31.  A 512-byte SF atom holds, for
+    // atom row r (0..31), 16 bytes = the 4-byte SF words of rows r, r+32,
+    // r+64, r+96; the MMA expects them replicated in every lane quadrant at
+    // columns +0..+3 (the tcgen05.cp 32x128b.warpx4 layout), so lane r of
+    // every warp loads those 16 bytes and stores them with tcgen05.st.
+    const int q = warp - C::W_SFW;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const int total = my_units * n_stages;
+    uint32_t stage = 0, phase = 0;
+    for (int g = 0; g < total; ++g) {
+      const uint32_t par = (uint32_t)g & 1u;
+      mbar_wait_a(a_full + stage * 8, phase);
+      mbar_wait_a(a_sf_free + par * 8, (((uint32_t)g >> 1) & 1u) ^ 1u);
+      tc_fence_after();
+      const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES + lane * 16;
+      const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES + lane * 16;
+      const uint32_t col = lane_base + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
+      {
+        uint32_t r[C::SFA_COLS];
+#pragma unroll
+        for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
+          const uint4 w = ld_shared_u32x4(sfa_s + at * 512);
+          r[at * 4 + 0] = w.x; r[at * 4 + 1] = w.y; r[at * 4 + 2] = w.z; r[at * 4 + 3] = w.w;
+        }
+        tmem_st<C::SFA_COLS>(col, r);
+      }
+      {
+        uint32_t r[C::SFB_COLS];
+#pragma unroll
+        for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at)
+#pragma unroll
+          for (int rb = 0; rb < BN / 128; ++rb) {
+            const uint4 w = ld_shared_u32x4(sfb_s + rb * C::SFA_BYTES + at * 512);
+            const int c = at * 4 * (BN / 128) + rb * 4;
+            r[c + 0] = w.x; r[c + 1] = w.y; r[c + 2] = w.z; r[c + 3] = w.w;
+          }
+        tmem_st<C::SFB_COLS>(col + C::SFA_COLS, r);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_a(a_sf_ready + par * 8);
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
   } else if (warp == C::W_SIG) {
     // ===================== sigma producer (MBS) =====================
@@ -556,24 +643,29 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
       const int m0 = mb * BM, n0 = nb * BN;
       const int row = m0 + row_in_tile;
-      float acc[COLS];
       if (!MBS || (p.dbg & 3)) {
+        // Plain: drain the accumulator 32 columns at a time (scale by the
+        // NVFP4 tensor scales, convert, store); the TMEM buffer is released
+        // right after its last tcgen05.ld.
         mbar_wait_a(a_tfull + buf * 8, tphase);
         tc_fence_after();
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < COLS; c += 32) {
           float v[32];
           tmem_ld32(tmem_lane + buf * BN + c, v);
           tmem_wait_ld();
+          if (c + 32 == COLS) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
+          }
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c + i] = v[i] * scale_nv;
+          for (int i = 0; i < 32; ++i) v[i] *= scale_nv;
+          store_row32<OUT_BF16>(p, row, n0 + half * COLS + c, v);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
         if (++buf == NB) { buf = 0; tphase ^= 1; }
       } else if constexpr (MBS) {
-        static_assert(COLS == 32, "MBS epilogue: 32 columns per thread");
+        float acc[COLS];
 #pragma unroll
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
         const uint32_t sig_row = a_smem + C::OFF_SIG + row_in_tile * 4;
@@ -587,14 +679,14 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           mbar_wait_a(a_tfull + buf * 8, tphase);
           tc_fence_after();
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int h = 0; h < COLS / 16; ++h) {
             float v[16];
             tmem_ld16(tmem_lane + buf * BN + h * 16, v);
             float4 sb[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) sb[q] = ld_shared_f32x4(sig + (h * 16 + q * 4) * 4);
             tmem_wait_ld();
-            if (h == 1) {
+            if (h == COLS / 16 - 1) {
               // TMEM buffer and sigma slot are free once P is in registers.
               tc_fence_before();
               __syncwarp();
@@ -617,38 +709,12 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           if (++buf == NB) { buf = 0; tphase ^= 1; }
           if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
         }
-      }
-      // ---- store ----
-      if (row < p.M) {
-        const int col0 = n0 + half * COLS;
-        if constexpr (OUT_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
-          if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
 #pragma unroll
-            for (int c = 0; c < COLS; c += 8) {
-              uint4 w;
-              w.x = pack_bf16x2(acc[c + 0], acc[c + 1]);
-              w.y = pack_bf16x2(acc[c + 2], acc[c + 3]);
-              w.z = pack_bf16x2(acc[c + 4], acc[c + 5]);
-              w.w = pack_bf16x2(acc[c + 6], acc[c + 7]);
-              *reinterpret_cast<uint4*>(out + c) = w;
-            }
-          } else {
+        for (int c = 0; c < COLS; c += 32) {
+          float v[32];
 #pragma unroll
-            for (int c = 0; c < COLS; ++c)
-              if (col0 + c < p.N) out[c] = __float2bfloat16_rn(acc[c]);
-          }
-        } else {
-          float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col0;
-          if (col0 + COLS <= p.N && (p.ldc % 4) == 0) {
-#pragma unroll
-            for (int c = 0; c < COLS; c += 4)
-              *reinterpret_cast<float4*>(out + c) = make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < COLS; ++c)
-              if (col0 + c < p.N) out[c] = acc[c];
-          }
+          for (int i = 0; i < 32; ++i) v[i] = acc[c + i];
+          store_row32<OUT_BF16>(p, row, n0 + half * COLS + c, v);
         }
       }
     }
