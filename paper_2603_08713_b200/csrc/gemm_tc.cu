@@ -375,14 +375,19 @@ struct Cfg {
   static constexpr int SIG_SLOT = (BM + BN) * 4;
   static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
   static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + 4;  // + sf_ready[2], sf_free[2]
+  // TMEM scale-factor buffers: as many as fit beside the accumulators (<= 4),
+  // so the SF writers run up to NSFB-1 stages ahead of the MMAs.
+  static constexpr int SF_COLS_STAGE = SF_ATOMS_PER_STAGE * 4 * (1 + BN / 128);
+  static constexpr int NSFB_FIT = (512 - NB * BN) / SF_COLS_STAGE;
+  static constexpr int NSFB = NSFB_FIT >= 4 ? 4 : (NSFB_FIT >= 2 ? 2 : 1);
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + 2 * 4;  // + sf_ready[], sf_free[]
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
   static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
   // TMEM columns: NB accumulators of BN columns, then 2 parity sets of SF.
   static constexpr int SFA_COLS = SF_ATOMS_PER_STAGE * 4;
   static constexpr int SFB_COLS = SF_ATOMS_PER_STAGE * 4 * (BN / 128);
   static constexpr int COL_SF = NB * BN;
-  static constexpr int TMEM_COLS_USED = COL_SF + 2 * (SFA_COLS + SFB_COLS);
+  static constexpr int TMEM_COLS_USED = COL_SF + NSFB * (SFA_COLS + SFB_COLS);
   static constexpr int TMEM_COLS = 512;
   // 8 epilogue warps: 2 per TMEM lane quadrant, BN/2 columns each.
   static constexpr int EPIW = 8;
@@ -408,8 +413,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
   uint64_t* sfull = tempty + NB;
   uint64_t* sempty = sfull + C::NSIG;
   uint64_t* sf_ready = sempty + C::NSIG;  // [2] SF parity buffer written (4 SF-writer warps)
-  uint64_t* sf_free = sf_ready + 2;        // [2] SF parity buffer consumed (MMA commit)
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sf_free + 2);
+  uint64_t* sf_free = sf_ready + 4;        // [NSFB] SF buffer consumed (MMA commit)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sf_free + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Work units: a cluster of CL CTAs takes CL consecutive 128-row blocks of
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       mbar_init(&sfull[b], 1);
       mbar_init(&sempty[b], C::EPIW);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < C::NSFB; ++b) {
       mbar_init(&sf_ready[b], NUM_SFW_WARPS);
       mbar_init(&sf_free[b], 1);
     }
@@ -509,9 +514,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       int s = 0, kstep = 0, in_chunk = 0;
       bool open = false;
       for (int g = 0; g < total; ++g) {
-        const uint32_t par = (uint32_t)g & 1u;
+        const uint32_t par = (uint32_t)g % C::NSFB;
         mbar_wait_a(a_full + stage * 8, phase);
-        mbar_wait_a(a_sf_ready + par * 8, ((uint32_t)g >> 1) & 1u);
+        mbar_wait_a(a_sf_ready + par * 8, ((uint32_t)g / C::NSFB) & 1u);
         tc_fence_after();
         const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
         const uint32_t sfb_col = sfa_col + C::SFA_COLS;
@@ -571,9 +576,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     const int total = my_units * n_stages;
     uint32_t stage = 0, phase = 0;
     for (int g = 0; g < total; ++g) {
-      const uint32_t par = (uint32_t)g & 1u;
+      const uint32_t par = (uint32_t)g % C::NSFB;
       mbar_wait_a(a_full + stage * 8, phase);
-      mbar_wait_a(a_sf_free + par * 8, (((uint32_t)g >> 1) & 1u) ^ 1u);
+      mbar_wait_a(a_sf_free + par * 8, (((uint32_t)g / C::NSFB) & 1u) ^ 1u);
       tc_fence_after();
       const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES + lane * 16;
       const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES + lane * 16;
@@ -679,14 +684,15 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           mbar_wait_a(a_tfull + buf * 8, tphase);
           tc_fence_after();
 #pragma unroll
-          for (int h = 0; h < COLS / 16; ++h) {
-            float v[16];
-            tmem_ld16(tmem_lane + buf * BN + h * 16, v);
-            float4 sb[4];
+          for (int h = 0; h < COLS / 32; ++h) {
+            float v[32];
+            tmem_ld16(tmem_lane + buf * BN + h * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
+            tmem_ld16(tmem_lane + buf * BN + h * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
+            float4 sb[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) sb[q] = ld_shared_f32x4(sig + (h * 16 + q * 4) * 4);
+            for (int q = 0; q < 8; ++q) sb[q] = ld_shared_f32x4(sig + (h * 32 + q * 4) * 4);
             tmem_wait_ld();
-            if (h == COLS / 16 - 1) {
+            if (h == COLS / 32 - 1) {
               // TMEM buffer and sigma slot are free once P is in registers.
               tc_fence_before();
               __syncwarp();
@@ -697,11 +703,11 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
             }
             // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < 8; ++q) {
               float w0, w1, w2, w3;
               mul2(w0, w1, sa, sb[q].x, sb[q].y);
               mul2(w2, w3, sa, sb[q].z, sb[q].w);
-              const int c = h * 16 + q * 4;
+              const int c = h * 32 + q * 4;
               fma2(acc[c], acc[c + 1], w0, w1, v[q * 4], v[q * 4 + 1]);
               fma2(acc[c + 2], acc[c + 3], w2, w3, v[q * 4 + 2], v[q * 4 + 3]);
             }
