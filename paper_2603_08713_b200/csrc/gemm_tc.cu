@@ -99,6 +99,19 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait that lets the hardware suspend the warp (up to `ns`) instead of
+// re-polling: for waits that are long by construction (the epilogue waiting
+// for a whole mainloop, the producer waiting for a free stage), so the
+// spinning warps do not steal issue slots from the MMA issuer.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -328,7 +341,7 @@ constexpr int TRACE_CHUNKS = 512;
 // the M x N bounds; 16-byte vector stores when the run is in bounds.
 template <bool OUT_BF16>
 __device__ __forceinline__ void store_row32(const Params& p, int row, int col0, const float (&v)[32]) {
-  if (row >= p.M) return;
+  if (row >= p.M || (p.dbg & 4)) return;
   if constexpr (OUT_BF16) {
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
     if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
@@ -484,7 +497,12 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         const uint8_t* sb = p.sfb + (int64_t)(n0 / 128) * p.sfb_kg * 512;
         for (int s = 0; s < n_stages; ++s) {
           const uint32_t fb = a_full + stage * 8;
-          mbar_wait_a(a_empty + stage * 8, phase ^ 1);
+          mbar_wait_sleep(a_empty + stage * 8, phase ^ 1);
+          if (p.dbg & 8) {  // experiment: no loads at all
+            mbar_arrive_a(fb);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx_a(fb, C::TX_BYTES);
           tma_load_2d_a(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
           if constexpr (CL == 1) {
@@ -515,7 +533,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       bool open = false;
       for (int g = 0; g < total; ++g) {
         const uint32_t par = (uint32_t)g % C::NSFB;
-        mbar_wait_a(a_full + stage * 8, phase);
+        // sf_ready implies full: the SF writers waited for this stage's TMA
+        // transaction (A, B and scale bytes) before writing the SF to TMEM.
         mbar_wait_a(a_sf_ready + par * 8, ((uint32_t)g / C::NSFB) & 1u);
         tc_fence_after();
         const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
@@ -583,7 +602,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES + lane * 16;
       const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES + lane * 16;
       const uint32_t col = lane_base + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
-      {
+      if (!(p.dbg & 16)) {
         uint32_t r[C::SFA_COLS];
 #pragma unroll
         for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
@@ -592,7 +611,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         }
         tmem_st<C::SFA_COLS>(col, r);
       }
-      {
+      if (!(p.dbg & 16)) {
         uint32_t r[C::SFB_COLS];
 #pragma unroll
         for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at)
@@ -604,7 +623,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           }
         tmem_st<C::SFB_COLS>(col + C::SFA_COLS, r);
       }
-      tmem_wait_st();
+      if (!(p.dbg & 16)) tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_a(a_sf_ready + par * 8);
@@ -652,7 +671,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         // Plain: drain the accumulator 32 columns at a time (scale by the
         // NVFP4 tensor scales, convert, store); the TMEM buffer is released
         // right after its last tcgen05.ld.
-        mbar_wait_a(a_tfull + buf * 8, tphase);
+        mbar_wait_sleep(a_tfull + buf * 8, tphase);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < COLS; c += 32) {

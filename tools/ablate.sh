@@ -1,7 +1,7 @@
 #!/bin/bash
 # GEMM timing experiments (dev only; modes 1/2 change numerics on purpose)
 export PYTHONPATH=$PWD
-for f in ${FLAGS:-0 1 2}; do
+for f in ${FLAGS:-0 4 8 16 28}; do
   echo "== MXQ_GEMM_DBG=$f"
   MXQ_GEMM_DBG=$f timeout 60 python - <<'PY'
 import torch, paper_2603_08713_b200 as M
