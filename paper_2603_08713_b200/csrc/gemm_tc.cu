@@ -393,6 +393,9 @@ struct Cfg {
   static constexpr int SF_COLS_STAGE = SF_ATOMS_PER_STAGE * 4 * (1 + BN / 128);
   static constexpr int NSFB_FIT = (512 - NB * BN) / SF_COLS_STAGE;
   static constexpr int NSFB = NSFB_FIT >= 4 ? 4 : (NSFB_FIT >= 2 ? 2 : 1);
+  // When every smem stage has its own SF buffer, the SF writers reuse the
+  // stage's `empty` barrier (MMA completion) instead of a separate commit.
+  static constexpr bool SF_ON_EMPTY = (NSFB == STAGES);
   static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + 2 * 4;  // + sf_ready[], sf_free[]
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
   static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
@@ -569,7 +572,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         }
         if constexpr (CL == 1) tc_commit_a(a_empty + stage * 8);
         else tc_commit_mc(a_empty + stage * 8, (uint16_t)((1u << CL) - 1));
-        tc_commit_a(a_sf_free + par * 8);
+        if constexpr (!C::SF_ON_EMPTY) tc_commit_a(a_sf_free + par * 8);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++s == n_stages) {  // tile done
           s = 0;
@@ -597,7 +600,13 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     for (int g = 0; g < total; ++g) {
       const uint32_t par = (uint32_t)g % C::NSFB;
       mbar_wait_a(a_full + stage * 8, phase);
-      mbar_wait_a(a_sf_free + par * 8, (((uint32_t)g / C::NSFB) & 1u) ^ 1u);
+      if constexpr (C::SF_ON_EMPTY) {
+        // buffer `par` == smem stage `stage`: its previous user is the MMA of
+        // stage g - STAGES, whose completion is the empty phase before this one
+        if (g >= STAGES) mbar_wait_a(a_empty + stage * 8, phase ^ 1);
+      } else {
+        mbar_wait_a(a_sf_free + par * 8, (((uint32_t)g / C::NSFB) & 1u) ^ 1u);
+      }
       tc_fence_after();
       const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES + lane * 16;
       const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES + lane * 16;
@@ -917,8 +926,8 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
     const int macro = ma ? a.macro_size : b.macro_size;
     if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
     if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
-    if (c_dtype == MXQ_BF16) return launch_variant<128, 5, 3, false, true, true, 2>(a, b, c, ldc, true, st);
-    return launch_variant<128, 5, 3, false, true, false, 2>(a, b, c, ldc, true, st);
+    if (c_dtype == MXQ_BF16) return launch_variant<128, 4, 3, false, true, true, 2>(a, b, c, ldc, true, st);
+    return launch_variant<128, 4, 3, false, true, false, 2>(a, b, c, ldc, true, st);
   }
   if (sf32) {
     if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, true, false, true, 2>(a, b, c, ldc, true, st);
