@@ -337,6 +337,25 @@ struct Params {
 
 constexpr int TRACE_CHUNKS = 512;
 
+// Store COLS consecutive bf16 columns (packed pairs) of one row, masked.
+template <int COLS>
+__device__ __forceinline__ void store_row_bf16(const Params& p, int row, int col0, const uint32_t (&pk)[COLS / 2]) {
+  if (row >= p.M || (p.dbg & 4)) return;
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
+  if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
+#pragma unroll
+    for (int c = 0; c < COLS / 2; c += 4)
+      *reinterpret_cast<uint4*>(out + 2 * c) = make_uint4(pk[c], pk[c + 1], pk[c + 2], pk[c + 3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < COLS / 2; ++c) {
+      const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&pk[c]);
+      if (col0 + 2 * c < p.N) out[2 * c] = h.x;
+      if (col0 + 2 * c + 1 < p.N) out[2 * c + 1] = h.y;
+    }
+  }
+}
+
 // Store 32 consecutive output columns of one row (f32 or bf16), masked to
 // the M x N bounds; 16-byte vector stores when the run is in bounds.
 template <bool OUT_BF16>
@@ -406,7 +425,7 @@ struct Cfg {
   static constexpr int TMEM_COLS_USED = COL_SF + NSFB * (SFA_COLS + SFB_COLS);
   static constexpr int TMEM_COLS = 512;
   // 8 epilogue warps: 2 per TMEM lane quadrant, BN/2 columns each.
-  static constexpr int EPIW = 8;
+  static constexpr int EPIW = 16;
   static constexpr int THREADS = (EPIW + NUM_SFW_WARPS + NUM_CTRL_WARPS) * 32;
   static constexpr int W_SFW = EPIW;  // first SF-writer warp (warpgroup aligned)
   static constexpr int W_TMA = EPIW + 7, W_MMA = EPIW + 6, W_SIG = EPIW + 5;
@@ -682,6 +701,23 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         // right after its last tcgen05.ld.
         mbar_wait_sleep(a_tfull + buf * 8, tphase);
         tc_fence_after();
+        if constexpr (OUT_BF16) {
+          // drain every column into packed bf16 registers, release TMEM, then
+          // store: the next tile's MMAs start while this tile is written out.
+          uint32_t pk[COLS / 2];
+#pragma unroll
+          for (int c = 0; c < COLS; c += 16) {
+            float v[16];
+            tmem_ld16(tmem_lane + buf * BN + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) pk[(c + i) / 2] = pack_bf16x2(v[i] * scale_nv, v[i + 1] * scale_nv);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
+          store_row_bf16<COLS>(p, row, n0 + half * COLS, pk);
+        } else
 #pragma unroll 1
         for (int c = 0; c < COLS; c += 32) {
           float v[32];
@@ -712,15 +748,14 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           mbar_wait_a(a_tfull + buf * 8, tphase);
           tc_fence_after();
 #pragma unroll
-          for (int h = 0; h < COLS / 32; ++h) {
-            float v[32];
-            tmem_ld16(tmem_lane + buf * BN + h * 32, *reinterpret_cast<float(*)[16]>(&v[0]));
-            tmem_ld16(tmem_lane + buf * BN + h * 32 + 16, *reinterpret_cast<float(*)[16]>(&v[16]));
-            float4 sb[8];
+          for (int h = 0; h < COLS / 16; ++h) {
+            float v[16];
+            tmem_ld16(tmem_lane + buf * BN + h * 16, v);
+            float4 sb[4];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) sb[q] = ld_shared_f32x4(sig + (h * 32 + q * 4) * 4);
+            for (int q = 0; q < 4; ++q) sb[q] = ld_shared_f32x4(sig + (h * 16 + q * 4) * 4);
             tmem_wait_ld();
-            if (h == COLS / 32 - 1) {
+            if (h == COLS / 16 - 1) {
               // TMEM buffer and sigma slot are free once P is in registers.
               tc_fence_before();
               __syncwarp();
@@ -731,11 +766,11 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
             }
             // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 4; ++q) {
               float w0, w1, w2, w3;
               mul2(w0, w1, sa, sb[q].x, sb[q].y);
               mul2(w2, w3, sa, sb[q].z, sb[q].w);
-              const int c = h * 32 + q * 4;
+              const int c = h * 16 + q * 4;
               fma2(acc[c], acc[c + 1], w0, w1, v[q * 4], v[q * 4 + 1]);
               fma2(acc[c + 2], acc[c + 3], w2, w3, v[q * 4 + 2], v[q * 4 + 3]);
             }
@@ -818,6 +853,16 @@ static long long* g_trace = nullptr;
 // Development experiments (MXQ_GEMM_DBG, read once): 1 = switch the MBS
 // accumulator per chunk without the epilogue hand-off, 2 = no switch either.
 // Both change numerics on purpose; 0 (unset) is the product path.
+// TMA-multicast cluster size for the GEMM (MXQ_GEMM_CL=1 disables; dev A/B).
+static int cluster_size() {
+  static int v = -1;
+  if (v < 0) {
+    const char* d = getenv("MXQ_GEMM_CL");
+    v = (d && atoi(d) == 1) ? 1 : 2;
+  }
+  return v;
+}
+
 static int debug_flags() {
   static int v = -1;
   if (v < 0) {
@@ -926,16 +971,16 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
     const int macro = ma ? a.macro_size : b.macro_size;
     if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
     if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
-    if (c_dtype == MXQ_BF16) return launch_variant<128, 4, 3, false, true, true, 2>(a, b, c, ldc, true, st);
-    return launch_variant<128, 4, 3, false, true, false, 2>(a, b, c, ldc, true, st);
+    if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<128, 4, 3, false, true, true, 1>(a, b, c, ldc, true, st) : launch_variant<128, 4, 3, false, true, true, 2>(a, b, c, ldc, true, st));
+    return (cluster_size() == 1 ? launch_variant<128, 4, 3, false, true, false, 1>(a, b, c, ldc, true, st) : launch_variant<128, 4, 3, false, true, false, 2>(a, b, c, ldc, true, st));
   }
   if (sf32) {
-    if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, true, false, true, 2>(a, b, c, ldc, true, st);
-    return launch_variant<256, 4, 1, true, false, false, 2>(a, b, c, ldc, true, st);
+    if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, false, true, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, false, true, 2>(a, b, c, ldc, true, st));
+    return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, false, false, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, false, false, 2>(a, b, c, ldc, true, st));
   }
   const bool ue8m0 = !nva;
-  if (c_dtype == MXQ_BF16) return launch_variant<256, 4, 1, false, false, true, 2>(a, b, c, ldc, ue8m0, st);
-  return launch_variant<256, 4, 1, false, false, false, 2>(a, b, c, ldc, ue8m0, st);
+  if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, false, false, true, 1>(a, b, c, ldc, ue8m0, st) : launch_variant<256, 4, 1, false, false, true, 2>(a, b, c, ldc, ue8m0, st));
+  return (cluster_size() == 1 ? launch_variant<256, 4, 1, false, false, false, 1>(a, b, c, ldc, ue8m0, st) : launch_variant<256, 4, 1, false, false, false, 2>(a, b, c, ldc, ue8m0, st));
 }
 
 }  // namespace mxq
