@@ -553,8 +553,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const int chunk_len = MBS ? p.macro_steps : (1 << 30);
       int s = 0, kstep = 0, in_chunk = 0;
       bool open = false;
-      uint32_t tchunk = 0;
-      long long* tr = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
       for (int g = 0; g < total; ++g) {
         const uint32_t par = (uint32_t)g % C::NSFB;
         // sf_ready implies full: the SF writers waited for this stage's TMA
@@ -573,11 +571,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
                 tc_commit_a(a_tfull + buf * 8);
                 if (++buf == NB) { buf = 0; tphase ^= 1; }
               }
-              if (tr && tchunk < TRACE_CHUNKS) tr[tchunk * 4 + 0] = clock64();
               mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
               tc_fence_after();
-              if (tr && tchunk < TRACE_CHUNKS) tr[tchunk * 4 + 1] = clock64();
-              ++tchunk;
               open = true;
             }
             uint32_t idesc = p.idesc;
@@ -744,52 +739,43 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
         const uint32_t sig_row = a_smem + C::OFF_SIG + row_in_tile * 4;
         const uint32_t sig_col = a_smem + C::OFF_SIG + (BM + half * COLS) * 4;
-        static_assert(COLS == 32, "pipelined MBS epilogue: two 16-column groups per chunk");
-        // Software pipeline: one 16-column TMEM load is always in flight while
-        // the previous group is folded in, across chunk boundaries too.
-        float va[16], vb[16];
-        if (p.n_chunks > 0) {
-          mbar_wait_a(a_tfull + buf * 8, tphase);
-          tc_fence_after();
-          tmem_ld16(tmem_lane + buf * BN, va);
-        }
 #pragma unroll 1
         for (int t = 0; t < p.n_chunks; ++t) {
+          // sigma slot of this chunk (landed long ago) and the partial P.
           mbar_wait_a(a_sfull + slot * 8, sphase);
           const uint32_t sig = sig_col + slot * C::SIG_SLOT;
           const float sa = ld_shared_f32(sig_row + slot * C::SIG_SLOT);
-          tmem_wait_ld();                                 // va = P[t][0:16)
-          tmem_ld16(tmem_lane + buf * BN + 16, vb);       // P[t][16:32) in flight
+          mbar_wait_a(a_tfull + buf * 8, tphase);
+          tc_fence_after();
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 sb = ld_shared_f32x4(sig + q * 16);
-            float w0, w1, w2, w3;
-            mul2(w0, w1, sa, sb.x, sb.y);
-            mul2(w2, w3, sa, sb.z, sb.w);
-            fma2(acc[q * 4], acc[q * 4 + 1], w0, w1, va[q * 4], va[q * 4 + 1]);
-            fma2(acc[q * 4 + 2], acc[q * 4 + 3], w2, w3, va[q * 4 + 2], va[q * 4 + 3]);
+          for (int h = 0; h < COLS / 16; ++h) {
+            float v[16];
+            tmem_ld16(tmem_lane + buf * BN + h * 16, v);
+            float4 sb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) sb[q] = ld_shared_f32x4(sig + (h * 16 + q * 4) * 4);
+            tmem_wait_ld();
+            if (h == COLS / 16 - 1) {
+              // TMEM buffer and sigma slot are free once P is in registers.
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) {
+                mbar_arrive_a(a_tempty + buf * 8);
+                mbar_arrive_a(a_sempty + slot * 8);
+              }
+            }
+            // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float w0, w1, w2, w3;
+              mul2(w0, w1, sa, sb[q].x, sb[q].y);
+              mul2(w2, w3, sa, sb[q].z, sb[q].w);
+              const int c = h * 16 + q * 4;
+              fma2(acc[c], acc[c + 1], w0, w1, v[q * 4], v[q * 4 + 1]);
+              fma2(acc[c + 2], acc[c + 3], w2, w3, v[q * 4 + 2], v[q * 4 + 3]);
+            }
           }
-          tmem_wait_ld();                                 // vb = P[t][16:32)
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);  // TMEM buffer t is free
           if (++buf == NB) { buf = 0; tphase ^= 1; }
-          if (t + 1 < p.n_chunks) {                       // next chunk's first group in flight
-            mbar_wait_a(a_tfull + buf * 8, tphase);
-            tc_fence_after();
-            tmem_ld16(tmem_lane + buf * BN, va);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 sb = ld_shared_f32x4(sig + 64 + q * 16);
-            float w0, w1, w2, w3;
-            mul2(w0, w1, sa, sb.x, sb.y);
-            mul2(w2, w3, sa, sb.z, sb.w);
-            fma2(acc[16 + q * 4], acc[16 + q * 4 + 1], w0, w1, vb[q * 4], vb[q * 4 + 1]);
-            fma2(acc[16 + q * 4 + 2], acc[16 + q * 4 + 3], w2, w3, vb[q * 4 + 2], vb[q * 4 + 3]);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive_a(a_sempty + slot * 8);  // sigma slot t is free
           if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
         }
 #pragma unroll
@@ -943,7 +929,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.macro_steps = macro / KSTEP;
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.idesc = make_idesc(BN, ue8m0);
-  p.trace = g_trace;
+  p.trace = nullptr;
   p.dbg = debug_flags();
   const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
   int clusters = num_sms() / CL;
