@@ -202,6 +202,73 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Warp-converged issue helpers.  The producer / MMA roles run their loops with
+// all 32 lanes (so descriptors, addresses and counters stay warp-uniform and
+// live in uniform registers); one lane, picked by elect.sync inside the asm,
+// issues.  Issuing from an `if (lane == 0)` region instead makes ptxas wrap
+// every tcgen05.mma / TMA in an ELECT + R2UR.BROADCAST waterfall loop.
+// ---------------------------------------------------------------------------
+#define MXQ_ELECT "{\n\t.reg .pred e_;\n\telect.sync _|e_, 0xffffffff;\n\t@e_ "
+__device__ __forceinline__ void expect_tx_e(uint32_t bar, uint32_t bytes) {
+  asm volatile(MXQ_ELECT "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void arrive_e(uint32_t bar) {
+  asm volatile(MXQ_ELECT "mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_e(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(MXQ_ELECT
+               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+               "[%4];\n\t}" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc_e(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 uint16_t mask) {
+  asm volatile(MXQ_ELECT
+               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+               " [%0], [%1, {%2, %3}], [%4], %5;\n\t}" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_e(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(MXQ_ELECT "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
+                   dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit_e(uint32_t bar) {
+  asm volatile(MXQ_ELECT "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc_e(uint32_t bar, uint16_t mask) {
+  asm volatile(MXQ_ELECT
+               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+               "%1;\n\t}" ::"r"(bar),
+               "h"(mask)
+               : "memory");
+}
+template <bool SF32>
+__device__ __forceinline__ void mma_bs_e(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum, uint32_t sfa, uint32_t sfb) {
+  if constexpr (SF32) {
+    asm volatile(
+        "{\n\t.reg .pred p, e_;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e_, 0xffffffff;\n\t"
+        "@e_ tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e_;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e_, 0xffffffff;\n\t"
+        "@e_ tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
+        : "memory");
+  }
+}
+
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
 // start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48),
 // base offset [49,52), layout [61,64) (2 = 128B swizzle, 0 = none).
@@ -335,7 +402,6 @@ struct Params {
   int dbg;              // ablation flags (MXQ_GEMM_DBG, development only)
 };
 
-constexpr int TRACE_CHUNKS = 512;
 
 // Store COLS consecutive bf16 columns (packed pairs) of one row, masked.
 template <int COLS>
@@ -425,7 +491,7 @@ struct Cfg {
   static constexpr int TMEM_COLS_USED = COL_SF + NSFB * (SFA_COLS + SFB_COLS);
   static constexpr int TMEM_COLS = 512;
   // 8 epilogue warps: 2 per TMEM lane quadrant, BN/2 columns each.
-  static constexpr int EPIW = 16;
+  static constexpr int EPIW = MBS ? 8 : 16;  // MBS: 64 columns per thread (issue-bound epilogue)
   static constexpr int THREADS = (EPIW + NUM_SFW_WARPS + NUM_CTRL_WARPS) * 32;
   static constexpr int W_SFW = EPIW;  // first SF-writer warp (warpgroup aligned)
   static constexpr int W_TMA = EPIW + 7, W_MMA = EPIW + 6, W_SIG = EPIW + 5;
@@ -434,6 +500,18 @@ struct Cfg {
   static_assert(TMEM_COLS_USED <= 512, "TMEM budget");
   static_assert(SMEM <= 232448, "shared memory budget");
 };
+
+// Development trace (mxq_debug_set_trace): clock64 of hand-off events of
+// CTA 0, 8 slots per chunk index, first 512 chunks.
+#ifndef MXQ_GEMM_TRACE
+#define MXQ_GEMM_TRACE 0
+#endif
+__device__ __forceinline__ void trace_at(const Params& p, int chunk, int slot) {
+  if constexpr (MXQ_GEMM_TRACE) {
+    if (p.trace != nullptr && blockIdx.x == 0 && chunk < 512 && (threadIdx.x & 31) == 0)
+      p.trace[chunk * 8 + slot] = clock64();
+  }
+}
 
 template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
 __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::THREADS, 1)
@@ -509,55 +587,55 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
   const int my_units = unit0 < num_units ? (num_units - 1 - unit0) / unit_step + 1 : 0;
 
   if (warp == C::W_TMA) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      for (int unit = unit0; unit < num_units; unit += unit_step) {
-        const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
-        const int m0 = mb * BM, n0 = nb * BN;
-        const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * 512;
-        const uint8_t* sb = p.sfb + (int64_t)(n0 / 128) * p.sfb_kg * 512;
-        for (int s = 0; s < n_stages; ++s) {
-          const uint32_t fb = a_full + stage * 8;
-          mbar_wait_sleep(a_empty + stage * 8, phase ^ 1);
-          if (p.dbg & 8) {  // experiment: no loads at all
-            mbar_arrive_a(fb);
-            if (++stage == STAGES) { stage = 0; phase ^= 1; }
-            continue;
-          }
-          mbar_expect_tx_a(fb, C::TX_BYTES);
-          tma_load_2d_a(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
-          if constexpr (CL == 1) {
-            tma_load_2d_a(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, fb, s * (KSTAGE / 2), n0);
-          } else {
-            tma_load_2d_mc(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B + crank * (BN / CL) * (KSTAGE / 2), &tmB, fb,
-                           s * (KSTAGE / 2), n0 + (int)crank * (BN / CL), (uint16_t)((1u << CL) - 1));
-          }
-          bulk_load_a(a_smem + C::OFF_SFA + stage * C::SFA_BYTES, sa + (int64_t)s * C::SFA_BYTES, C::SFA_BYTES, fb);
-#pragma unroll
-          for (int rb = 0; rb < BN / 128; ++rb)
-            bulk_load_a(a_smem + C::OFF_SFB + stage * C::SFB_BYTES + rb * C::SFA_BYTES,
-                        sb + ((int64_t)rb * p.sfb_kg * 512 + (int64_t)s * C::SFA_BYTES), C::SFA_BYTES, fb);
+    // ===================== TMA producer (warp-converged) =====================
+    uint32_t stage = 0, phase = 0;
+    for (int unit = unit0; unit < num_units; unit += unit_step) {
+      const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
+      const int m0 = mb * BM, n0 = nb * BN;
+      const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * 512;
+      const uint8_t* sb = p.sfb + (int64_t)(n0 / 128) * p.sfb_kg * 512;
+      for (int s = 0; s < n_stages; ++s) {
+        const uint32_t fb = a_full + stage * 8;
+        mbar_wait_sleep(a_empty + stage * 8, phase ^ 1);
+        if (p.dbg & 8) {  // experiment: no loads at all
+          arrive_e(fb);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          continue;
         }
+        expect_tx_e(fb, C::TX_BYTES);
+        tma_load_2d_e(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
+        if constexpr (CL == 1) {
+          tma_load_2d_e(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, fb, s * (KSTAGE / 2), n0);
+        } else {
+          tma_load_2d_mc_e(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B + crank * (BN / CL) * (KSTAGE / 2), &tmB, fb,
+                           s * (KSTAGE / 2), n0 + (int)crank * (BN / CL), (uint16_t)((1u << CL) - 1));
+        }
+        bulk_load_e(a_smem + C::OFF_SFA + stage * C::SFA_BYTES, sa + (int64_t)s * C::SFA_BYTES, C::SFA_BYTES, fb);
+#pragma unroll
+        for (int rb = 0; rb < BN / 128; ++rb)
+          bulk_load_e(a_smem + C::OFF_SFB + stage * C::SFB_BYTES + rb * C::SFA_BYTES,
+                      sb + ((int64_t)rb * p.sfb_kg * 512 + (int64_t)s * C::SFA_BYTES), C::SFA_BYTES, fb);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == C::W_MMA) {
-    // ===================== MMA issuer =====================
+    // ===================== MMA issuer (warp-converged) =====================
     // Scale factors reach TMEM through the SF-writer warps (tcgen05.st), not
     // tcgen05.cp: the tensor pipe only runs MMAs.
-    if (lane == 0) {
+    {
       const int total = my_units * n_stages;
       uint32_t stage = 0, phase = 0;      // stage g in the smem ring
       uint32_t buf = 0, tphase = 0;       // accumulator ring position
       const int chunk_len = MBS ? p.macro_steps : (1 << 30);
-      int s = 0, kstep = 0, in_chunk = 0;
+      int s = 0, kstep = 0, in_chunk = 0, tchunk = 0;
       bool open = false;
       for (int g = 0; g < total; ++g) {
         const uint32_t par = (uint32_t)g % C::NSFB;
         // sf_ready implies full: the SF writers waited for this stage's TMA
         // transaction (A, B and scale bytes) before writing the SF to TMEM.
+        trace_at(p, tchunk, 4);
         mbar_wait_a(a_sf_ready + par * 8, ((uint32_t)g / C::NSFB) & 1u);
+        trace_at(p, tchunk, 5);
         tc_fence_after();
         const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
         const uint32_t sfb_col = sfa_col + C::SFA_COLS;
@@ -568,12 +646,15 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           if (kstep < n_ksteps) {
             if (in_chunk == 0) {
               if (open) {
-                tc_commit_a(a_tfull + buf * 8);
+                tc_commit_e(a_tfull + buf * 8);
                 if (++buf == NB) { buf = 0; tphase ^= 1; }
               }
+              trace_at(p, tchunk, 0);
               mbar_wait_a(a_tempty + buf * 8, tphase ^ 1);
+              trace_at(p, tchunk, 1);
               tc_fence_after();
               open = true;
+              ++tchunk;
             }
             uint32_t idesc = p.idesc;
             int atom = k;
@@ -583,22 +664,22 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
               idesc |= (sf_id << 29) | (sf_id << 4);
             }
             // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
-            mma_bs<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
-                         in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
+            mma_bs_e<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
+                           in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
             if (++in_chunk == chunk_len) in_chunk = 0;
           }
           ++kstep;
         }
-        if constexpr (CL == 1) tc_commit_a(a_empty + stage * 8);
-        else tc_commit_mc(a_empty + stage * 8, (uint16_t)((1u << CL) - 1));
-        if constexpr (!C::SF_ON_EMPTY) tc_commit_a(a_sf_free + par * 8);
+        if constexpr (CL == 1) tc_commit_e(a_empty + stage * 8);
+        else tc_commit_mc_e(a_empty + stage * 8, (uint16_t)((1u << CL) - 1));
+        if constexpr (!C::SF_ON_EMPTY) tc_commit_e(a_sf_free + par * 8);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++s == n_stages) {  // tile done
           s = 0;
           kstep = 0;
           in_chunk = 0;
           if (open) {
-            tc_commit_a(a_tfull + buf * 8);
+            tc_commit_e(a_tfull + buf * 8);
             if (++buf == NB) { buf = 0; tphase ^= 1; }
           }
           open = false;
@@ -654,7 +735,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       if (!(p.dbg & 16)) tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_a(a_sf_ready + par * 8);
+      arrive_e(a_sf_ready + par * 8);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
   } else if (warp == C::W_SIG) {
@@ -662,7 +743,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     // One slot per chunk: sigmaA[128 rows] and sigmaB[BN cols] as f32 (a
     // non-MBS operand points at a row of ones with ld 0).
     if constexpr (MBS) {
-      if (lane == 0 && !(p.dbg & 3)) {
+      if (!(p.dbg & 3)) {
         uint32_t slot = 0, sphase = 0;
         for (int unit = unit0; unit < num_units; unit += unit_step) {
           const int m0 = ((unit % groups_m) * CL + (int)crank) * BM, n0 = (unit / groups_m) * BN;
@@ -670,11 +751,11 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
           for (int t = 0; t < p.n_chunks; ++t) {
             const uint32_t fb = a_sfull + slot * 8;
-            mbar_wait_a(a_sempty + slot * 8, sphase ^ 1);
-            mbar_expect_tx_a(fb, (BM + BN) * 4);
+            mbar_wait_sleep(a_sempty + slot * 8, sphase ^ 1);
+            expect_tx_e(fb, (BM + BN) * 4);
             const uint32_t dst = a_smem + C::OFF_SIG + slot * C::SIG_SLOT;
-            bulk_load_a(dst, ga + (int64_t)t * p.sga_ld, BM * 4, fb);
-            bulk_load_a(dst + BM * 4, gb + (int64_t)t * p.sgb_ld, BN * 4, fb);
+            bulk_load_e(dst, ga + (int64_t)t * p.sga_ld, BM * 4, fb);
+            bulk_load_e(dst + BM * 4, gb + (int64_t)t * p.sgb_ld, BN * 4, fb);
             if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
           }
         }
@@ -689,6 +770,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     const int row_in_tile = quad * 32 + lane;
     const uint32_t tmem_lane = tmem + ((uint32_t)(quad * 32) << 16) + half * COLS;
     uint32_t buf = 0, tphase = 0, slot = 0, sphase = 0;
+    int echunk = 0;
     float scale_nv = 1.0f;
     if (p.tsa && p.tsb) scale_nv = (float)(*p.tsa * *p.tsb);
     for (int unit = unit0; unit < num_units; unit += unit_step) {
@@ -742,10 +824,13 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
 #pragma unroll 1
         for (int t = 0; t < p.n_chunks; ++t) {
           // sigma slot of this chunk (landed long ago) and the partial P.
+          if (lane == 0 && e == 0) trace_at(p, echunk, 2);
           mbar_wait_a(a_sfull + slot * 8, sphase);
           const uint32_t sig = sig_col + slot * C::SIG_SLOT;
           const float sa = ld_shared_f32(sig_row + slot * C::SIG_SLOT);
           mbar_wait_a(a_tfull + buf * 8, tphase);
+          if (lane == 0 && e == 0) trace_at(p, echunk, 3);
+          if (lane == 0 && e == C::EPIW - 1) trace_at(p, echunk, 7);
           tc_fence_after();
 #pragma unroll
           for (int h = 0; h < COLS / 16; ++h) {
@@ -762,6 +847,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
               if (lane == 0) {
                 mbar_arrive_a(a_tempty + buf * 8);
                 mbar_arrive_a(a_sempty + slot * 8);
+                if (e == 0) trace_at(p, echunk, 6);
               }
             }
             // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
@@ -777,6 +863,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           }
           if (++buf == NB) { buf = 0; tphase ^= 1; }
           if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
+          ++echunk;
         }
 #pragma unroll
         for (int c = 0; c < COLS; c += 32) {
@@ -929,7 +1016,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.macro_steps = macro / KSTEP;
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.idesc = make_idesc(BN, ue8m0);
-  p.trace = nullptr;
+  p.trace = g_trace;
   p.dbg = debug_flags();
   const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
   int clusters = num_sms() / CL;

@@ -15,16 +15,22 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t 
   return d;
 }
 
-template <int N, bool SF32>
-__global__ void k(int iters, int commit_every, long long* out) {
+template <int N, bool SF32, bool WARP>
+__global__ void k(int iters, int commit_every, long long* out, int ld_mode) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t ring[4];
   __shared__ __align__(8) uint64_t bar_final;
+  __shared__ volatile int stop;
   const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) stop = 0;
   for (int i = threadIdx.x; i < 65536; i += blockDim.x) smem[i] = 0;
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&bar)));
+    for (int r = 0; r < 4; ++r)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&ring[r])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"((uint32_t)__cvta_generic_to_shared(&bar_final)));
   }
   if (warp == 0) {
@@ -47,7 +53,20 @@ __global__ void k(int iters, int commit_every, long long* out) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   long long t0 = 0, t1 = 0;
-  if (threadIdx.x == 0) {
+  if (warp >= 4) {
+    const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 128 + ((warp / 4) & 3) * 32;
+    float acc = 0.f;
+    while (!stop) {
+      uint32_t r[16];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]),"=r"(r[1]),"=r"(r[2]),"=r"(r[3]),"=r"(r[4]),"=r"(r[5]),"=r"(r[6]),"=r"(r[7]),"=r"(r[8]),"=r"(r[9]),"=r"(r[10]),"=r"(r[11]),"=r"(r[12]),"=r"(r[13]),"=r"(r[14]),"=r"(r[15]) : "r"(taddr) : "memory");
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc += __uint_as_float(r[j]);
+    }
+    if (acc == 12345.f) out[2] = 1;
+  }
+  if (WARP ? (warp == 0) : (threadIdx.x == 0)) {
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
     const uint64_t ad = desc(sb, 16, 1024, 2), bd = desc(sb + 16384, 16, 1024, 2);
     uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(128 >> 4) << 24);
@@ -61,20 +80,45 @@ __global__ void k(int iters, int commit_every, long long* out) {
           "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
           :: "r"(tmem), "l"(ad + kk * 2), "l"(bd + kk * 2), "r"(idesc), "r"(1), "r"(tmem + 256), "r"(tmem + 300));
       } else {
+        if (WARP) {
+          asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+            :: "r"(tmem), "l"(ad + kk * 2), "l"(bd + kk * 2), "r"(idesc), "r"(1), "r"(tmem + 256), "r"(tmem + 300));
+        } else {
         asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
           "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
           :: "r"(tmem), "l"(ad + kk * 2), "l"(bd + kk * 2), "r"(idesc), "r"(1), "r"(tmem + 256), "r"(tmem + 300));
+        }
       }
-      if (commit_every && ((i + 1) % commit_every == 0)) {
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(bar_a) : "memory");
+      if (ld_mode > 0) {  // spin ld_mode cycles between MMAs
+        const long long w0 = clock64();
+        while (clock64() - w0 < ld_mode) { }
+      }
+      if (commit_every > 0 && ((i + 1) % commit_every == 0)) {
+        if (WARP) asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" :: "r"(bar_a) : "memory");
+        else asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(bar_a) : "memory");
+      }
+      if (commit_every < 0 && ((i + 1) % (-commit_every) == 0)) {
+        // ring of 4 barriers; before reusing one, wait for its previous phase (real pipeline use)
+        const int c = (i + 1) / (-commit_every) - 1;
+        const uint32_t rb = (uint32_t)__cvta_generic_to_shared(&ring[c & 3]);
+        if (c >= 4) {
+          const uint32_t par = (uint32_t)((c / 4 - 1) & 1);
+          asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" :: "r"(rb), "r"(par) : "memory");
+        }
+        if (WARP) asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" :: "r"(rb) : "memory");
+        else asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(rb) : "memory");
       }
     }
+    const long long t_issue = clock64();
     const uint32_t fin = (uint32_t)__cvta_generic_to_shared(&bar_final);
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(fin) : "memory");
+    if (WARP) asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" :: "r"(fin) : "memory");
+    else asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(fin) : "memory");
     asm volatile("{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" :: "r"(fin), "r"(0) : "memory");
     t1 = clock64();
+    stop = 1;
     (void)ph;
-    if (blockIdx.x == 0) out[0] = t1 - t0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { out[0] = t1 - t0; out[1] = t_issue - t0; }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -84,17 +128,20 @@ __global__ void k(int iters, int commit_every, long long* out) {
   }
 }
 
-template <int N, bool SF32>
-void run(int iters, int commit_every) {
-  long long* d; cudaMalloc(&d, 8);
-  auto kern = k<N, SF32>;
+template <int N, bool SF32, bool WARP = false>
+void run(int iters, int commit_every, int ld_warps = 0, int delay = 0) {
+  long long* d; cudaMalloc(&d, 32);
+  auto kern = k<N, SF32, WARP>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  kern<<<148, 128, 65536>>>(iters, commit_every, d);
+  kern<<<148, 128 + 32 * ld_warps, 65536>>>(iters, commit_every, d, delay);
   cudaDeviceSynchronize();
-  kern<<<148, 128, 65536>>>(iters, commit_every, d);
+  kern<<<148, 128 + 32 * ld_warps, 65536>>>(iters, commit_every, d, delay);
   cudaError_t e = cudaDeviceSynchronize();
-  long long c = 0; cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  long long cc[2] = {0, 0}; cudaMemcpy(cc, d, 16, cudaMemcpyDeviceToHost);
+  long long c = cc[0];
+  printf("[issue %lld] ", cc[1]);
   double macs = (double)iters * 128 * N * 64;
+  printf("%s delay=%d ld_warps=%d ", WARP ? "warp" : "thread", delay, ld_warps);
   printf("N=%d %s commit_every=%d: %lld cyc for %d MMAs -> %.0f MACs/clk/SM (%.1f cyc/MMA) %s\n", N,
          SF32 ? "mxf4.block32" : "mxf4nvf4.block16", commit_every, c, iters, macs / c, (double)c / iters,
          e == cudaSuccess ? "" : cudaGetErrorString(e));
@@ -102,13 +149,16 @@ void run(int iters, int commit_every) {
 }
 
 int main() {
-  run<256, false>(4096, 0);
-  run<256, false>(4096, 16);
-  run<256, false>(4096, 4);
-  run<256, false>(4096, 2);
-  run<256, false>(4096, 1);
-  run<128, false>(4096, 0);
-  run<128, false>(4096, 2);
-  run<256, true>(4096, 0);
+  run<256, false, false>(4096, 0);
+  run<256, false, true>(4096, 0);
+  run<128, false, false>(4096, 0);
+  run<128, false, true>(4096, 0);
+  run<128, false, true>(4096, 0, 0, 30);
+  run<128, false, true>(4096, 2);
+  run<128, false, true>(4096, -2);
+  run<256, false, true>(4096, 4);
+  run<256, false, true>(4096, -4);
+  run<256, false, true>(4096, -1);
+  run<256, true, true>(4096, -4);
   return 0;
 }
