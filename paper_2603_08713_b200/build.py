@@ -29,6 +29,8 @@ FLAGS = [
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
 ]
+# Development builds only (e.g. MXQ_NVCC_EXTRA=-DMXQ_GEMM_TRACE=1 for tools/trace_mbs.py).
+FLAGS += os.environ.get("MXQ_NVCC_EXTRA", "").split()
 
 
 def _digest() -> str:
