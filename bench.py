@@ -359,7 +359,8 @@ def run_ours(args):
             traffic = None
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(fp4_peak, 1), "unit": "TFLOP/s",
                 "frac": round(achieved / fp4_peak, 4), "traffic": traffic, "peak_basis": basis,
-                "kernel": "k_gemm_tc<128,5,3,mxf4nvf4 UE8M0,MBS,bf16>",
+                "kernel": "k_gemm_tc<BN=128,STAGES=4,NB=3,mxf4nvf4.block16 UE8M0,MBS,bf16,CL=2>",
+                "traffic_basis": "profiles/gemm_traffic.json: ncu --set full DRAM bytes per launch, mean of the same 4 layer launches",
                 "algorithmic": "2*M*N*K per launch over the 4 layer launches, CUDA events on the launch stream"}
 
     # ---- CPU baseline: the reference algorithm (oracle port) on a sample ---

@@ -1,0 +1,27 @@
+"""The bench's four Llama-3-8B MBS-H layer GEMMs (M=4096), each launched twice,
+for `ncu --set full -k regex:k_gemm_tc --launch-skip 4 --launch-count 4`:
+the second round is what gets captured (warm TMA descriptors, weights in HBM).
+Writes nothing; profiles/gemm_traffic.json is assembled from the ncu report."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2603_08713_b200 as M
+
+V = M.Variant
+LAYERS = [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 28672, 4096), ("down", 4096, 14336)]
+arm = sys.argv[1] if len(sys.argv) > 1 else "mbs_h"
+pairs = {"mbs_h": (V.MBS_S, V.MBS_D), "ocp32": (V.OCP32, V.OCP32), "mx16_oas": (V.MX16_OAS, V.MX16_OAS),
+         "nvfp4": (V.NVFP4, V.NVFP4)}
+va, vw = pairs[arm]
+g = torch.Generator(device="cuda").manual_seed(0)
+ops = []
+for name, n, k in LAYERS:
+    a = torch.randn(4096, k, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    ops.append((M.quantize_tensor(a, M.SchemeConfig(va)), M.quantize_tensor(w, M.SchemeConfig(vw))))
+torch.cuda.synchronize()
+for _ in range(2):
+    for aq, wq in ops:
+        M.matmul_quantized(aq, wq, out_dtype=torch.bfloat16)
+torch.cuda.synchronize()
+print("done")
