@@ -1,0 +1,557 @@
+// gemm_mbs.cu -- tcgen05 MBS GEMM (K8) for sm_100a.   C[M,N] = A[M,K] . B[N,K]^T
+//
+// Replaces matmul_quantized (src/gemm.py:137-172) for operand pairs where at
+// least one side carries the MBS macro factor sigma = 1/(1+m8/256) per (row,
+// macro of 128 K) (src/quantize.py:383-406; per-chunk semantics SPEC.md:325;
+// the paper's Appendix E epilogue).  sigma is not a power of
+// two, so it cannot ride in the UE8M0 block scales of the block-scaled MMA:
+// every macro chunk is MMA'd (kind::mxf4nvf4.block16, UE8M0) into its own
+// TMEM partial buffer P and the epilogue folds acc += (sigmaA_i*sigmaB_j) * P_ij
+// in registers, two FP32 operations per output per chunk.
+//
+// That FP32 work bounds the kernel: 128 FP32 lanes/clk/SM against 16384 FP4
+// MACs/clk/SM means 2*BM*BN/128 cycles of FP32 per chunk versus BM*BN*128/16384
+// of MMA -- the tensor pipe can be at most 50 % busy.  The
+// structure is chosen so that nothing else binds first:
+//   * 128 x 192 tiles, N=192 MMAs (96 cycles each, long enough to hide the
+//     issuing thread's ~70-cycle per-MMA cost that made N=128 MMAs issue-bound),
+//     two 192-column TMEM partial buffers and two 48-column scale-factor
+//     buffers (384 + 2*64 columns <= 512);
+//   * 16 epilogue warps (4 per TMEM lane quadrant, 48 columns each) hold the
+//     48 f32 accumulators and load a chunk's whole partial (48 registers) before
+//     releasing its TMEM buffer, so the next-but-one chunk's MMAs start early;
+//     setmaxnreg gives them 112 registers and the 4 control warps 32 (the pool is
+//     the 96 x 640 registers allocated at launch);
+//   * the epilogue warps also move each stage's scale factors smem -> TMEM
+//     (tcgen05.st, 3 atoms per warp per stage): tcgen05.cp costs ~64 tensor-pipe
+//     cycles per 512-byte atom (tools/microbench_cp.cu) and dedicated writer
+//     warps would cost the registers the accumulators need;
+//   * clusters of 2 CTAs share the B tile by TMA multicast.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdlib.h>
+
+#include "mxq_arith.cuh"
+#include "mxq_internal.h"
+#include "tc_ptx.cuh"
+
+namespace mxq {
+namespace mbs {
+
+using namespace tc;
+
+constexpr int BM = 128;
+constexpr int KSTAGE = 256, KSTEP = 64;     // K elements per pipeline stage / per MMA
+constexpr int NSFB = 2, NSIG = 8;
+constexpr int EPIW = 16;                    // epilogue warps (4 per TMEM lane quadrant)
+constexpr int W_TMA = 16, W_MMA = 17;       // control warpgroup: warps 16..19
+constexpr int THREADS = 20 * 32;
+constexpr int ATOM = 512;                   // SF atom: 128 rows x 4 blocks of 16
+constexpr int STAGE_A = BM * KSTAGE / 2;    // 16 KB of A codes per stage
+constexpr int SFA_BYTES = 4 * ATOM;         // 4 k-steps
+
+// Tile shape (BN output columns, NB TMEM partial buffers).  The product path
+// is BN=192, NB=2 (DESIGN.md section 3 lists the measured alternatives).
+template <int BN_, int NB_>
+struct MbsCfg {
+  static constexpr int BN = BN_, NB = NB_;
+  static constexpr int COLS = BN / 4;                   // output columns per epilogue thread
+  static constexpr int NRB = BN / 128 + (BN % 128 ? 1 : 0);  // 128-row SF atoms a tile can touch
+  static constexpr int STAGES = BN > 128 ? 4 : 5;
+  static constexpr int STAGE_B = BN * KSTAGE / 2;
+  static constexpr int SFB_BYTES = NRB * 4 * ATOM;     // NRB row blocks x 4 k-steps
+  static constexpr int SIG_SLOT = (BM + BN) * 4;       // sigmaA[128] + sigmaB[BN], f32
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * STAGE_A;
+  static constexpr int OFF_SFA = OFF_B + STAGES * STAGE_B;
+  static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
+  static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
+  static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + NSFB;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
+  // TMEM: partial buffers [0, NB*BN), SF buffers 64-aligned after them
+  // (misaligned SF addresses slow the MMA, tools/microbench_mma3.cu).  Within
+  // an SF buffer: SFA of k-step j at +4j, SFB (NRB 128-row atoms) at +16+4*NRB*j.
+  static constexpr int COL_SF0 = (NB * BN + 63) / 64 * 64;
+  static constexpr int SF_STRIDE = 64;
+  // 16*32*EPI + 4*32*CTRL must fit the 96 x 640 registers allocated at launch
+  static constexpr bool SETMAXNREG = COLS > 32;
+  static constexpr int EPI_REGS = 112, CTRL_REGS = 32;
+  static_assert(SMEM <= 232448, "shared memory budget");
+  static_assert(OFF_B % 1024 == 0 && STAGE_B % 1024 == 0 && (BN / 2) * 128 % 1024 == 0, "128B-swizzle alignment");
+  static_assert(COL_SF0 + NSFB * SF_STRIDE <= 512, "TMEM budget");
+  static_assert(16 + 4 * NRB * 4 <= SF_STRIDE, "SF buffer");
+};
+
+struct Params {
+  const uint8_t* sfa;  // scale-factor atoms [rows/128][sf_kg][512]
+  const uint8_t* sfb;
+  int64_t sfa_kg, sfb_kg;
+  int sfb_rb;          // allocated 128-row blocks of B's SF atoms
+  const float* sga;    // sigma^T (n_macros, ld) f32; a non-MBS side points at a ones row with ld 0
+  const float* sgb;
+  int64_t sga_ld, sgb_ld;
+  void* c;
+  int64_t ldc;
+  int M, N, K;
+  int mac_steps;       // macro size / 64
+  int n_chunks;        // macros per row
+  uint32_t idesc;
+  long long* trace;    // clock64 trace of CTA 0 (MXQ_GEMM_TRACE builds only)
+};
+
+#ifndef MXQ_GEMM_TRACE
+#define MXQ_GEMM_TRACE 0
+#endif
+// 16 clock64 slots per chunk of CTA 0, first 512 chunks (tools/trace_mbs.py).
+__device__ __forceinline__ void trace_at(const Params& p, uint32_t chunk, int slot) {
+  if constexpr (MXQ_GEMM_TRACE) {
+    if (p.trace != nullptr && blockIdx.x == 0 && chunk < 512 && (threadIdx.x & 31) == 0)
+      p.trace[chunk * 16 + slot] = clock64();
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
+template <int R>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint4 w) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(w.x), "r"(w.y), "r"(w.z),
+               "r"(w.w)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a.x),
+               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init_a(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
+// Start a 16-column TMEM load without waiting (the caller waits once for all).
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, float* v) {
+  uint32_t* r = reinterpret_cast<uint32_t*>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
+// Pin values produced by tcgen05.ld behind tcgen05.wait::ld: the arithmetic
+// below is ordinary (non-volatile) asm/C++ that the compiler could otherwise
+// hoist above the wait.
+template <int N>
+__device__ __forceinline__ void reg_fence(float* v) {
+#pragma unroll
+  for (int i = 0; i < N; i += 8)
+    asm volatile("" : "+f"(v[i]), "+f"(v[i + 1]), "+f"(v[i + 2]), "+f"(v[i + 3]), "+f"(v[i + 4]), "+f"(v[i + 5]),
+                 "+f"(v[i + 6]), "+f"(v[i + 7]));
+}
+
+template <int BN_, int NB_, bool OUT_BF16, int CL>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+  using C = MbsCfg<BN_, NB_>;
+  constexpr int BN = C::BN, NB = C::NB, STAGES = C::STAGES, COLS = C::COLS, NRB = C::NRB;
+  constexpr int STAGE_B = C::STAGE_B, SFB_BYTES = C::SFB_BYTES, SIG_SLOT = C::SIG_SLOT;
+  constexpr int OFF_A = C::OFF_A, OFF_B = C::OFF_B, OFF_SFA = C::OFF_SFA, OFF_SFB = C::OFF_SFB;
+  constexpr int OFF_SIG = C::OFF_SIG, OFF_BAR = C::OFF_BAR, COL_SF0 = C::COL_SF0, SF_STRIDE = C::SF_STRIDE;
+  extern __shared__ uint8_t smem_raw[];
+  // 32-bit shared-window addresses only (a generic 64-bit base gets
+  // rematerialised inside the hot loops under register pressure).
+  const uint32_t a_smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t a_full = a_smem + OFF_BAR, a_empty = a_full + 8 * STAGES;
+  const uint32_t a_tfull = a_empty + 8 * STAGES, a_tempty = a_tfull + 8 * NB;
+  const uint32_t a_sfull = a_tempty + 8 * NB, a_sempty = a_sfull + 8 * NSIG;
+  const uint32_t a_sfready = a_sempty + 8 * NSIG;
+  const uint32_t a_tmem_slot = a_sfready + 8 * NSFB;
+
+  // warp index through a shuffle so ptxas knows it is warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
+  const int groups_m = (tiles_m + CL - 1) / CL;
+  const int num_units = groups_m * tiles_n;
+  const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
+  uint32_t crank = 0;
+  if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int n_ksteps = (p.K + KSTEP - 1) / KSTEP;
+  const int n_stages = (p.K + KSTAGE - 1) / KSTAGE;
+  const int n_chunks = p.n_chunks, mac_steps = p.mac_steps;
+  const int my_units = unit0 < num_units ? (num_units - 1 - unit0) / unit_step + 1 : 0;
+  const int total_chunks = my_units * n_chunks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init_a(a_full + 8 * s, 1);
+      mbar_init_a(a_empty + 8 * s, CL);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init_a(a_tfull + 8 * b, 1);
+      mbar_init_a(a_tempty + 8 * b, EPIW);
+    }
+    for (int b = 0; b < NSIG; ++b) {
+      mbar_init_a(a_sfull + 8 * b, 1);
+      mbar_init_a(a_sempty + 8 * b, EPIW);
+    }
+    for (int b = 0; b < NSFB; ++b) mbar_init_a(a_sfready + 8 * b, EPIW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+  }
+  if (warp == W_MMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(a_tmem_slot) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = ld_shared_u32(a_tmem_slot);
+
+  if (warp >= EPIW) {
+    if constexpr (C::SETMAXNREG) setmaxnreg_dec<C::CTRL_REGS>();
+    if (warp == W_TMA) {
+      // ===================== TMA producer =====================
+      uint32_t st = 0, ph = 0, slot = 0, sph = 0;
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
+        const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
+        const int m0 = mb * BM, n0 = nb * BN;
+        const int rb0 = n0 / 128;
+        const int nrb = (rb0 + NRB <= p.sfb_rb) ? NRB : p.sfb_rb - rb0;
+        const uint32_t tx = STAGE_A + STAGE_B + SFA_BYTES + nrb * 4 * ATOM;
+        const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * ATOM;
+        const uint8_t* sb = p.sfb + (int64_t)rb0 * p.sfb_kg * ATOM;
+        const float* ga = p.sga + (p.sga_ld ? m0 : 0);
+        const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
+        int sb_bytes = BN * 4;
+        if (p.sgb_ld && p.sgb_ld - n0 < BN) sb_bytes = (int)(p.sgb_ld - n0) * 4;
+        int chunk = 0;
+        for (int s = 0; s < n_stages; ++s) {
+          const uint32_t fb = a_full + st * 8;
+          mbar_wait_a(a_empty + st * 8, ph ^ 1);
+          trace_at(p, (uint32_t)((unit - unit0) / unit_step * n_chunks + chunk), 12);
+          expect_tx_e(fb, tx);
+          tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, &tmA, fb, s * (KSTAGE / 2), m0);
+          if constexpr (CL == 1) {
+            tma_load_2d_e(a_smem + OFF_B + st * STAGE_B, &tmB, fb, s * (KSTAGE / 2), n0);
+          } else {
+            tma_load_2d_mc_e(a_smem + OFF_B + st * STAGE_B + crank * (BN / CL) * (KSTAGE / 2), &tmB, fb,
+                             s * (KSTAGE / 2), n0 + (int)crank * (BN / CL), (uint16_t)((1u << CL) - 1));
+          }
+          bulk_load_e(a_smem + OFF_SFA + st * SFA_BYTES, sa + (int64_t)s * SFA_BYTES, SFA_BYTES, fb);
+          for (int r = 0; r < nrb; ++r)
+            bulk_load_e(a_smem + OFF_SFB + st * SFB_BYTES + r * 4 * ATOM,
+                        sb + ((int64_t)r * p.sfb_kg + (int64_t)s * 4) * ATOM, 4 * ATOM, fb);
+          if (++st == STAGES) { st = 0; ph ^= 1; }
+          // sigma slices of the chunks that start in this stage
+          while (chunk < n_chunks && chunk * mac_steps < 4 * (s + 1)) {
+            const uint32_t sfb = a_sfull + slot * 8;
+            mbar_wait_a(a_sempty + slot * 8, sph ^ 1);
+            expect_tx_e(sfb, BM * 4 + sb_bytes);
+            const uint32_t dst = a_smem + OFF_SIG + slot * SIG_SLOT;
+            bulk_load_e(dst, ga + (int64_t)chunk * p.sga_ld, BM * 4, sfb);
+            bulk_load_e(dst + BM * 4, gb + (int64_t)chunk * p.sgb_ld, sb_bytes, sfb);
+            trace_at(p, (uint32_t)((unit - unit0) / unit_step * n_chunks + chunk), 11);
+            if (++slot == NSIG) { slot = 0; sph ^= 1; }
+            ++chunk;
+          }
+        }
+      }
+    } else if (warp == W_MMA) {
+      // ===================== MMA issuer =====================
+      uint32_t g = 0;  // global stage counter (smem ring and SF buffers)
+      uint32_t buf = 0, tph = 0;  // TMEM partial-buffer ring
+      uint32_t st = 0;
+      uint32_t q = 0;
+      for (int unit = unit0; unit < num_units; unit += unit_step) {
+        const int nb = unit / groups_m;
+        const uint32_t sfb_shift = ((nb * BN) % 128) ? 2u : 0u;  // odd 192-tiles start 64 rows into the atom
+        int ks = 0;
+        uint64_t adesc = 0, bdesc = 0;
+        uint32_t sfa_col = 0;
+        for (int c = 0; c < n_chunks; ++c, ++q) {
+          const uint32_t dcol = tmem + buf * BN;
+          trace_at(p, q, 0);
+          mbar_wait_a(a_tempty + buf * 8, tph ^ 1u);
+          trace_at(p, q, 1);
+          tc_fence_after();
+          int kend = (c + 1) * mac_steps;
+          if (kend > n_ksteps) kend = n_ksteps;
+          const int kbeg = ks;
+          for (; ks < kend; ++ks) {
+            const uint32_t j = (uint32_t)ks & 3u;
+            if (j == 0) {
+              mbar_wait_a(a_sfready + (g & (NSFB - 1)) * 8, (g / NSFB) & 1u);
+              trace_at(p, q, 10);
+              tc_fence_after();
+              adesc = operand_desc(a_smem + OFF_A + st * STAGE_A);
+              bdesc = operand_desc(a_smem + OFF_B + st * STAGE_B);
+              sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
+            }
+            mma_bs_e<false>(dcol, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), p.idesc, ks > kbeg ? 1u : 0u,
+                            sfa_col + 4 * j, sfa_col + 16 + 4 * NRB * j + sfb_shift);
+            if (j == 3 || ks + 1 == n_ksteps) {
+              if constexpr (CL == 1) tc_commit_e(a_empty + st * 8);
+              else tc_commit_mc_e(a_empty + st * 8, (uint16_t)((1u << CL) - 1));
+              ++g;
+              if (++st == STAGES) st = 0;
+            }
+          }
+          tc_commit_e(a_tfull + buf * 8);
+          trace_at(p, q, 2);
+          if (++buf == NB) { buf = 0; tph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 0..15) =====================
+    if constexpr (C::SETMAXNREG) setmaxnreg_inc<C::EPI_REGS>();
+    const int quad = warp & 3, grp = warp >> 2;
+    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
+    const uint32_t t_ld = t_lane + grp * COLS;
+    const int row_in_tile = quad * 32 + lane;
+    const uint32_t sig_a = a_smem + OFF_SIG + row_in_tile * 4;
+    const uint32_t sig_b = a_smem + OFF_SIG + (BM + grp * COLS) * 4;
+    // Scale factors of global stage `sf_next`: this warp moves k-step `grp`
+    // (one SFA atom, NRB SFB atoms) into its lane quadrant of SF buffer
+    // sf_next % 2, then arrives on sf_ready (16 arrivals per stage).
+    uint32_t sf_next = 0;
+    auto write_sf_upto = [&](uint32_t upto) {
+      while (sf_next <= upto) {
+        const uint32_t st = sf_next % STAGES;
+        mbar_wait_a(a_full + st * 8, (sf_next / STAGES) & 1u);
+        const uint32_t sf_lane = lane * 16 + grp * ATOM;
+        const uint4 wa = ld_shared_u32x4(a_smem + OFF_SFA + st * SFA_BYTES + sf_lane);
+        const uint4 wb0 = ld_shared_u32x4(a_smem + OFF_SFB + st * SFB_BYTES + sf_lane);
+        const uint32_t col = t_lane + COL_SF0 + (sf_next & (NSFB - 1)) * SF_STRIDE;
+        tmem_st4(col + 4 * grp, wa);
+        if constexpr (NRB == 2) {
+          const uint4 wb1 = ld_shared_u32x4(a_smem + OFF_SFB + st * SFB_BYTES + 4 * ATOM + sf_lane);
+          tmem_st8(col + 16 + 8 * grp, wb0, wb1);
+        } else {
+          tmem_st4(col + 16 + 4 * grp, wb0);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        arrive_e(a_sfready + (sf_next & (NSFB - 1)) * 8);
+        ++sf_next;
+      }
+    };
+    // Chunk q + NB (tile ordinal nx_t, chunk nx_c): the chunk whose MMAs the
+    // release of chunk q's partial buffer lets start.
+    int nx_t = 0, nx_c = 0;
+    auto nx_stage = [&]() -> uint32_t {
+      int last = (nx_c + 1) * mac_steps;
+      if (last > n_ksteps) last = n_ksteps;
+      return (uint32_t)(nx_t * n_stages + ((last - 1) >> 2));
+    };
+    auto nx_advance = [&]() {
+      if (++nx_c == n_chunks) { nx_c = 0; ++nx_t; }
+    };
+    if (total_chunks > 0) {
+      for (int i = 0; i < NB && i < total_chunks; ++i) {
+        write_sf_upto(nx_stage());
+        nx_advance();
+      }
+    }
+
+    // Load side (TMEM partial buffers) and compute side (sigma ring) counters.
+    uint32_t ql = 0, lbuf = 0, ltph = 0;   // next chunk to load
+    uint32_t qc = 0, slot = 0, sph = 0;    // next chunk to compute
+    auto start_load = [&](float* v) {
+      if (warp == 0) trace_at(p, ql, 3);
+      mbar_wait_a(a_tfull + lbuf * 8, ltph);
+      if (warp == 0) trace_at(p, ql, 4);
+      if (warp == EPIW - 1) trace_at(p, ql, 8);
+      tc_fence_after();
+      // chunk ql is complete, so every MMA of the stages before it is too: the
+      // SF buffer of chunk ql+NB's stage can be overwritten now (before the
+      // release below lets chunk ql+NB's MMAs start; they wait for these).
+      if ((int)ql + NB < total_chunks) {
+        write_sf_upto(nx_stage());
+        nx_advance();
+      }
+#pragma unroll
+      for (int h = 0; h < COLS / 16; ++h) tmem_ld16_nw(t_ld + lbuf * BN + h * 16, v + h * 16);
+    };
+    auto finish_load = [&](float* v) {
+      tmem_wait_ld();
+      reg_fence<COLS>(v);
+      tc_fence_before();
+      __syncwarp();
+      arrive_e(a_tempty + lbuf * 8);
+      if (warp == 0) trace_at(p, ql, 5);
+      ++ql;
+      if (++lbuf == NB) { lbuf = 0; ltph ^= 1; }
+    };
+    // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
+    auto compute = [&](float* acc, const float* v) {
+      mbar_wait_a(a_sfull + slot * 8, sph);
+      if (warp == 0) trace_at(p, qc, 6);
+      const uint32_t so = slot * SIG_SLOT;
+      const float sa = ld_shared_f32(sig_a + so);
+#pragma unroll
+      for (int i = 0; i < COLS; i += 4) {
+        const float4 sb = ld_shared_f32x4(sig_b + so + i * 4);
+        float w0, w1, w2, w3;
+        mul2(w0, w1, sa, sb.x, sb.y);
+        mul2(w2, w3, sa, sb.z, sb.w);
+        fma2(acc[i], acc[i + 1], w0, w1, v[i], v[i + 1]);
+        fma2(acc[i + 2], acc[i + 3], w2, w3, v[i + 2], v[i + 3]);
+      }
+      __syncwarp();
+      arrive_e(a_sempty + slot * 8);
+      if (warp == 0) trace_at(p, qc, 7);
+      if (warp == EPIW - 1) trace_at(p, qc, 9);
+      ++qc;
+      if (++slot == NSIG) { slot = 0; sph ^= 1; }
+    };
+
+    for (int unit = unit0; unit < num_units; unit += unit_step) {
+      const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
+      const int row = mb * BM + row_in_tile;
+      const int col0 = nb * BN + grp * COLS;
+      float acc[COLS];
+#pragma unroll
+      for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
+#pragma unroll 1
+      for (int c = 0; c < n_chunks; ++c) {
+        float v[COLS];
+        start_load(v);
+        finish_load(v);
+        compute(acc, v);
+      }
+      // store the tile row (masked to M x N)
+      if (row < p.M) {
+        if constexpr (OUT_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
+          if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
+#pragma unroll
+            for (int i = 0; i < COLS; i += 8) {
+              uint4 w;
+              w.x = pack_bf16x2(acc[i + 0], acc[i + 1]);
+              w.y = pack_bf16x2(acc[i + 2], acc[i + 3]);
+              w.z = pack_bf16x2(acc[i + 4], acc[i + 5]);
+              w.w = pack_bf16x2(acc[i + 6], acc[i + 7]);
+              *reinterpret_cast<uint4*>(out + i) = w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < COLS; ++i)
+              if (col0 + i < p.N) out[i] = __float2bfloat16_rn(acc[i]);
+          }
+        } else {
+          float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col0;
+          if (col0 + COLS <= p.N && (p.ldc % 4) == 0) {
+#pragma unroll
+            for (int i = 0; i < COLS; i += 4)
+              *reinterpret_cast<float4*>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < COLS; ++i)
+              if (col0 + i < p.N) out[i] = acc[i];
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync();
+  if (warp == W_MMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+template <int BN, int NB, bool OUT_BF16, int CL>
+static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStream_t st) {
+  using C = MbsCfg<BN, NB>;
+  constexpr int SMEM = C::SMEM;
+  auto kern = k_gemm_mbs<BN, NB, OUT_BF16, CL>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return set_cuda_error(e);
+    attr_set = true;
+  }
+  CUtensorMap ta, tb;
+  int rc = make_code_map(&ta, a.codes, a.rows, a.cols / 2, a.codes_ld, BM);
+  if (rc) return rc;
+  rc = make_code_map(&tb, b.codes, b.rows, b.cols / 2, b.codes_ld, BN / CL);
+  if (rc) return rc;
+  const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
+  const float* ones = ones_buffer();
+  if (!ones) return set_error(ERR_INVALID, "could not allocate the sigma ones row");
+  Params p{};
+  p.sfa = a.scales_mma;
+  p.sfb = b.scales_mma;
+  p.sfa_kg = a.sf_kpad / 4;
+  p.sfb_kg = b.sf_kpad / 4;
+  p.sfb_rb = (int)((b.rows + 255) / 256 * 2);
+  p.sga = ma ? a.sig_t : ones;
+  p.sgb = mbb ? b.sig_t : ones;
+  p.sga_ld = ma ? a.sig_t_ld : 0;
+  p.sgb_ld = mbb ? b.sig_t_ld : 0;
+  p.c = c;
+  p.ldc = ldc;
+  p.M = (int)a.rows;
+  p.N = (int)b.rows;
+  p.K = (int)a.cols;
+  const int macro = ma ? a.macro_size : b.macro_size;
+  p.mac_steps = macro / KSTEP;
+  p.n_chunks = (int)((a.cols + macro - 1) / macro);
+  // E2M1 x E2M1, UE8M0 scales, N = 192, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
+  p.trace = g_trace;
+  p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+  const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
+  int clusters = num_sms() / CL;
+  if (units < clusters) clusters = units;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CL);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  return check_launch();
+}
+
+}  // namespace mbs
+
+// MBS pair on the tcgen05 path: macro sizes 64, 128, 256 (two SF buffers
+// cover at most one stage of look-ahead; other sizes take the exact kernel).
+bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
+  const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
+  if (!ma && !mb) return false;
+  if (a.variant == NVFP4 || b.variant == NVFP4) return false;  // (an MBS operand makes the SF layout block-16)
+  const int macro = ma ? a.macro_size : b.macro_size;
+  if (ma && mb && a.macro_size != b.macro_size) return false;
+  return macro == 64 || macro == 128 || macro == 256;
+}
+
+int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
+  if (c_dtype == MXQ_BF16) return mbs::launch<192, 2, true, 2>(a, b, c, ldc, st);
+  return mbs::launch<192, 2, false, 2>(a, b, c, ldc, st);
+}
+
+}  // namespace mxq

@@ -29,6 +29,7 @@
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
+#include "tc_ptx.cuh"
 
 namespace mxq {
 namespace tc {
@@ -44,341 +45,6 @@ constexpr int STAGE_BYTES_A = BM * KSTAGE / 2;  // 16 KB
 // access.
 constexpr int NUM_CTRL_WARPS = 4;   // TMA producer, MMA issuer, sigma producer, spare
 constexpr int NUM_SFW_WARPS = 4;    // scale-factor writers (one per TMEM lane quadrant)
-
-// ---------------------------------------------------------------------------
-// PTX wrappers
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITA_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAITA_%=;\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-// Wait that lets the hardware suspend the warp (up to `ns`) instead of
-// re-polling: for waits that are long by construction (the epilogue waiting
-// for a whole mainloop, the producer waiting for a free stage), so the
-// spinning warps do not steal issue slots from the MMA issuer.
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAITS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WAITS_%=;\n\t}" ::"r"(bar),
-      "r"(parity), "r"(0x100000u)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_a(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_a(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_a(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_load_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
-      : "memory");
-}
-// MMA completion arrives on the barrier at the same smem offset in every CTA
-// of `mask` (each CTA's stage may be overwritten by a peer's multicast only
-// after every consumer in the cluster is done with it).
-__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                   bar),
-               "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit_a(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ uint4 ld_shared_u32x4(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
-  return v;
-}
-template <int N>
-__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&r)[N]) {
-  static_assert(N == 8 || N == 16 || N == 32, "tmem_st width");
-  if constexpr (N == 8) {
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
-                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-  } else if constexpr (N == 16) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-            taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-  } else {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
-        "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-        "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ float4 ld_shared_f32x4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
-}
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// Warp-converged issue helpers.  The producer / MMA roles run their loops with
-// all 32 lanes (so descriptors, addresses and counters stay warp-uniform and
-// live in uniform registers); one lane, picked by elect.sync inside the asm,
-// issues.  Issuing from an `if (lane == 0)` region instead makes ptxas wrap
-// every tcgen05.mma / TMA in an ELECT + R2UR.BROADCAST waterfall loop.
-// ---------------------------------------------------------------------------
-#define MXQ_ELECT "{\n\t.reg .pred e_;\n\telect.sync _|e_, 0xffffffff;\n\t@e_ "
-__device__ __forceinline__ void expect_tx_e(uint32_t bar, uint32_t bytes) {
-  asm volatile(MXQ_ELECT "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void arrive_e(uint32_t bar) {
-  asm volatile(MXQ_ELECT "mbarrier.arrive.shared::cta.b64 _, [%0];\n\t}" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_e(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
-  asm volatile(MXQ_ELECT
-               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-               "[%4];\n\t}" ::"r"(dst),
-               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_2d_mc_e(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
-                                                 uint16_t mask) {
-  asm volatile(MXQ_ELECT
-               "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-               " [%0], [%1, {%2, %3}], [%4], %5;\n\t}" ::"r"(dst),
-               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_load_e(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile(MXQ_ELECT "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(
-                   dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_commit_e(uint32_t bar) {
-  asm volatile(MXQ_ELECT "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_commit_mc_e(uint32_t bar, uint16_t mask) {
-  asm volatile(MXQ_ELECT
-               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
-               "%1;\n\t}" ::"r"(bar),
-               "h"(mask)
-               : "memory");
-}
-template <bool SF32>
-__device__ __forceinline__ void mma_bs_e(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accum, uint32_t sfa, uint32_t sfb) {
-  if constexpr (SF32) {
-    asm volatile(
-        "{\n\t.reg .pred p, e_;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e_, 0xffffffff;\n\t"
-        "@e_ tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
-            d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p, e_;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e_, 0xffffffff;\n\t"
-        "@e_ tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
-            d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
-        : "memory");
-  }
-}
-
-// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
-// start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48),
-// base offset [49,52), layout [61,64) (2 = 128B swizzle, 0 = none).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)(layout & 7u) << 61;
-  return d;
-}
-
-// K-major operand tile, 128-byte rows with the 128B swizzle, 8-row groups
-// 1024 bytes apart.  Advancing K inside the swizzle atom = start + bytes.
-__device__ __forceinline__ uint64_t operand_desc(uint32_t saddr) { return smem_desc(saddr, 16, 1024, 2); }
-
-// Scale-factor atom (32 rows x 16 B, 8-row core matrices 128 B apart).
-__device__ __forceinline__ uint64_t sf_desc(uint32_t saddr) { return smem_desc(saddr, 0, 128, 0); }
-
-__device__ __forceinline__ void utccp_sf(uint32_t tmem_col, uint64_t desc) {
-  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(tmem_col), "l"(desc) : "memory");
-}
-
-template <bool SF32>
-__device__ __forceinline__ void mma_bs(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accum, uint32_t sfa, uint32_t sfb) {
-  if constexpr (SF32) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
-            d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
-            d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
-        : "memory");
-  }
-}
-
-// 32 lanes x 32 consecutive 32-bit TMEM columns -> 32 registers per thread.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
-      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // .x = lo (low half)
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// acc{0,1} += (sa * sb{0,1}) * p{0,1} with packed f32x2 multiply / FMA
-// (FMUL2 + FFMA2): the MBS epilogue is bound by these two FP32 ops per output
-// per macro chunk.
-__device__ __forceinline__ void fma2_scaled(float& acc0, float& acc1, float sa, float sb0, float sb1, float p0,
-                                            float p1) {
-  asm("{\n\t.reg .b64 w, q, c, s;\n\t"
-      "mov.b64 w, {%2, %3};\n\t"
-      "mov.b64 s, {%6, %6};\n\t"
-      "mov.b64 q, {%4, %5};\n\t"
-      "mov.b64 c, {%0, %1};\n\t"
-      "mul.rn.f32x2 w, w, s;\n\t"
-      "fma.rn.f32x2 c, w, q, c;\n\t"
-      "mov.b64 {%0, %1}, c;\n\t}"
-      : "+f"(acc0), "+f"(acc1)
-      : "f"(sb0), "f"(sb1), "f"(p0), "f"(p1), "f"(sa));
-}
-
-// 32 lanes x 16 columns.
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr)
-      : "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-__device__ __forceinline__ void mul2(float& o0, float& o1, float a, float b0, float b1) {
-  asm("{\n\t.reg .b64 x, y;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %4};\n\t"
-      "mul.rn.f32x2 x, x, y;\n\tmov.b64 {%0, %1}, x;\n\t}"
-      : "=f"(o0), "=f"(o1)
-      : "f"(b0), "f"(b1), "f"(a));
-}
-
-__device__ __forceinline__ void fma2(float& acc0, float& acc1, float w0, float w1, float p0, float p1) {
-  asm("{\n\t.reg .b64 w, q, c;\n\tmov.b64 w, {%2, %3};\n\tmov.b64 q, {%4, %5};\n\t"
-      "mov.b64 c, {%0, %1};\n\tfma.rn.f32x2 c, w, q, c;\n\tmov.b64 {%0, %1}, c;\n\t}"
-      : "+f"(acc0), "+f"(acc1)
-      : "f"(w0), "f"(w1), "f"(p0), "f"(p1));
-}
 
 // ---------------------------------------------------------------------------
 // Kernel parameters
@@ -906,7 +572,7 @@ static PFN_encodeTiled get_encode() {
 
 // 2-D map over packed codes: inner dim = K/2 bytes, outer = rows; box =
 // 128 bytes x box_rows, 128B swizzle; out-of-bounds reads fill zeros.
-static int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t kbytes, int64_t ld,
+int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t kbytes, int64_t ld,
                          int box_rows) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return set_error(ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
@@ -935,7 +601,7 @@ static uint32_t make_idesc(int n, bool ue8m0) {
   return d;
 }
 
-static long long* g_trace = nullptr;
+long long* g_trace = nullptr;
 
 // Development experiments (MXQ_GEMM_DBG, read once): 1 = switch the MBS
 // accumulator per chunk without the epilogue hand-off, 2 = no switch either.
@@ -950,6 +616,18 @@ static int cluster_size() {
   return v;
 }
 
+// First-generation MBS kernel (128x128 tiles, N=128 MMAs): the path for
+// macro sizes the 192-column kernel does not take, or forced with
+// MXQ_GEMM_MBS_V1=1 for A/B timing (development).
+static bool mbs_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* d = getenv("MXQ_GEMM_MBS_V1");
+    v = (d && atoi(d) == 1) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 static int debug_flags() {
   static int v = -1;
   if (v < 0) {
@@ -960,7 +638,7 @@ static int debug_flags() {
 }
 
 // 256 f32 ones per device: the sigma row of a non-MBS operand in an MBS GEMM.
-static const float* ones_buffer() {
+const float* ones_buffer() {
   static float* ptrs[64] = {nullptr};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1058,6 +736,7 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
     const int macro = ma ? a.macro_size : b.macro_size;
     if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
     if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
+    if (gemm_mbs_supported(a, b) && !mbs_v1()) return launch_gemm_mbs(a, b, c, c_dtype, ldc, st);
     if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<128, 4, 3, false, true, true, 1>(a, b, c, ldc, true, st) : launch_variant<128, 4, 3, false, true, true, 2>(a, b, c, ldc, true, st));
     return (cluster_size() == 1 ? launch_variant<128, 4, 3, false, true, false, 1>(a, b, c, ldc, true, st) : launch_variant<128, 4, 3, false, true, false, 2>(a, b, c, ldc, true, st));
   }

@@ -29,6 +29,8 @@ int launch_gemm_exact(const QDesc* a, const QDesc* b, const float* fa, int64_t l
                       int64_t m, int64_t n, int64_t k, float* c, int64_t ldc, uint32_t* status, cudaStream_t st);
 int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, uint32_t* status,
                    cudaStream_t st);
+bool gemm_mbs_supported(const QDesc& a, const QDesc& b);
+int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st);
 void set_gemm_trace(long long* p);
 int launch_build_gemm_layout(const QDesc& q, int sf_block, cudaStream_t st);
 

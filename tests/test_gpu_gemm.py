@@ -90,3 +90,37 @@ def test_tk_validation_like_reference():
     with pytest.raises(ValueError):
         M.matmul_quantized(qm, qm, M.TileConfig(8, 8, 64))
     M.matmul_quantized(qm, qm, M.TileConfig(8, 8, 256))
+
+
+@pytest.mark.parametrize("macro", [64, 128, 256, 512])
+def test_tc_gemm_mbs_macro_sizes(macro):
+    """The 192-column MBS kernel takes macros 64/128/256 (512 runs the
+    first-generation kernel); partial last macro at K = 2880."""
+    rng = np.random.Generator(np.random.PCG64(11 + macro))
+    for (m, n, k) in [(200, 500, 1024), (130, 384, 2880)]:
+        a = rng.standard_t(4, (m, k)).astype(np.float32)
+        b = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+        aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S, macro_size=macro))
+        bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant.MBS_D, macro_size=macro))
+        c = M.matmul_quantized(aq, bq, M.TileConfig(t_k=max(macro, 128))).cpu().numpy()
+        qa = O.quantize(a, "mbs_s", macro_size=macro)
+        qb = O.quantize(b, "mbs_d", macro_size=macro)
+        da, db = O.dequantize(qa).astype(np.float64), O.dequantize(qb).astype(np.float64)
+        _check(c, da @ db.T, np.abs(da) @ np.abs(db).T, ("macro", macro, m, n, k))
+
+
+@pytest.mark.parametrize("va,vb", [("mbs_s", "mbs_d"), ("mbs_s", "mx16_oas"), ("ocp32", "mbs_d")])
+def test_tc_gemm_mbs_persistent_tiles(va, vb):
+    """More tiles than CTAs: each CTA runs several 128x192 tiles back to back
+    (TMEM buffer / SF buffer / sigma ring phases carried across tiles)."""
+    rng = np.random.Generator(np.random.PCG64(21))
+    m, n, k = 2048, 3072, 384
+    a = rng.standard_t(4, (m, k)).astype(np.float32)
+    b = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+    aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant(va)))
+    bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant(vb)))
+    c = M.matmul_quantized(aq, bq).cpu().numpy()
+    want, bound = _ref(a, b, va, vb)
+    _check(c, want, bound, (va, vb, "persistent"))
+    cb = M.matmul_quantized(aq, bq, out_dtype=torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
