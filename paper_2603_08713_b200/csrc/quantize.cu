@@ -16,6 +16,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
 
@@ -60,38 +62,6 @@ __device__ __forceinline__ float block_absmax(const float (&v)[N], bool& finite)
   }
   finite = !bad;
   return a;
-}
-
-// Codes for N scaled values: scaled = v * sf (exact power-of-two f32 scaling;
-// a result that would be f32-subnormal is < 2^-126 and encodes to 0 either
-// way), packed two per byte, even element in the low nibble.
-template <int N>
-__device__ __forceinline__ void encode_block(const float (&v)[N], float sf, uint32_t (&packed)[N / 8]) {
-#pragma unroll
-  for (int w = 0; w < N / 8; ++w) {
-    uint32_t word = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float lo = __fmul_rn(v[w * 8 + 2 * j], sf);
-      float hi = __fmul_rn(v[w * 8 + 2 * j + 1], sf);
-      word |= e2m1x2(lo, hi) << (8 * j);
-    }
-    packed[w] = word;
-  }
-}
-
-template <int N>
-__device__ __forceinline__ void store_codes(uint8_t* __restrict__ dst, const uint32_t (&packed)[N / 8]) {
-  if constexpr (N == 16) {
-    *reinterpret_cast<uint2*>(dst) = make_uint2(packed[0], packed[1]);
-  } else {
-    *reinterpret_cast<uint4*>(dst) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-  }
-}
-
-__device__ __forceinline__ void store_scale(const QDesc& q, int64_t r, int64_t kb, uint8_t s) {
-  if (q.scales) q.scales[r * q.scales_ld + kb] = s;
-  if (q.scales_mma) q.scales_mma[sf_mma_offset(r, kb, q.sf_kpad)] = s;
 }
 
 // ---------------------------------------------------------------------------
@@ -145,10 +115,13 @@ struct Blk16 {
 template <int DT>
 __device__ __forceinline__ void ld_blk(const void* __restrict__ x, int64_t off, Blk16<DT>& b) {
   if constexpr (DT == DT_BF16) {
-    const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(x) + off);
-    const uint4 a0 = __ldcs(p), a1 = __ldcs(p + 1);
-    b.w[0] = a0.x; b.w[1] = a0.y; b.w[2] = a0.z; b.w[3] = a0.w;
-    b.w[4] = a1.x; b.w[5] = a1.y; b.w[6] = a1.z; b.w[7] = a1.w;
+    // one 256-bit load per 16-element block (sm_100 LDG.256): a warp reads 1 KB
+    // contiguous per instruction; no L1 allocation for the streamed input
+    const uint16_t* p = reinterpret_cast<const uint16_t*>(x) + off;
+    asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(b.w[0]), "=r"(b.w[1]), "=r"(b.w[2]), "=r"(b.w[3]), "=r"(b.w[4]), "=r"(b.w[5]),
+                   "=r"(b.w[6]), "=r"(b.w[7])
+                 : "l"(p));
   } else {
     const uint4* p = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(x) + off);
 #pragma unroll
@@ -218,65 +191,6 @@ __device__ __forceinline__ void enc16(const float (&v)[16], float sf, uint32_t (
 __device__ __forceinline__ void store_scale(const QDesc& q, uint32_t r, uint32_t kb, uint8_t s) {
   if (q.scales) q.scales[(int64_t)r * q.scales_ld + kb] = s;
   if (q.scales_mma) q.scales_mma[sf_mma_offset(r, kb, q.sf_kpad)] = s;
-}
-
-// One 16-block of MX16 / MX16_OAS.
-template <int DT, bool OAS>
-__device__ __forceinline__ void do_blk16(const Blk16<DT>& b, const QDesc& q, uint32_t r, uint32_t kb,
-                                         uint32_t& bad) {
-  const float alpha = blk_absmax<DT>(b, bad);
-  const uint8_t biased = e8m0_biased_16(alpha, OAS);
-  float v[16];
-  blk_f32<DT>(b, v);
-  uint32_t codes[2];
-  enc16(v, exp2i_f32(127 - (int)biased), codes);
-  *reinterpret_cast<uint2*>(q.codes + (int64_t)r * q.codes_ld + kb * 8) = make_uint2(codes[0], codes[1]);
-  store_scale(q, r, kb, biased);
-}
-
-// K1a: MX16 / MX16_OAS (block 16).  Thread = two blocks per iteration.
-template <int DT, bool OAS>
-__global__ void __launch_bounds__(256) k_quantize_mx16(const void* __restrict__ x, int64_t x_ld, QDesc q,
-                                                       FastDiv fd_nbr, uint32_t nb, uint32_t* __restrict__ status) {
-  uint32_t bad = 0;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t b0 = blockIdx.x * blockDim.x + threadIdx.x; b0 < nb; b0 += 2 * stride) {
-    const uint32_t b1 = b0 + stride;
-    const uint32_t r0 = fdiv(b0, fd_nbr), k0 = b0 - r0 * fd_nbr.d;
-    const uint32_t r1 = fdiv(b1, fd_nbr), k1 = b1 - r1 * fd_nbr.d;
-    Blk16<DT> x0, x1;
-    ld_blk<DT>(x, (int64_t)r0 * x_ld + k0 * 16, x0);
-    if (b1 < nb) ld_blk<DT>(x, (int64_t)r1 * x_ld + k1 * 16, x1);
-    do_blk16<DT, OAS>(x0, q, r0, k0, bad);
-    if (b1 < nb) do_blk16<DT, OAS>(x1, q, r1, k1, bad);
-  }
-  if (bad) atomicOr(status, ST_NONFINITE);
-}
-
-// K1b: OCP32 (block 32 = two 16-element halves sharing one scale).
-template <int DT>
-__global__ void __launch_bounds__(256) k_quantize_ocp32(const void* __restrict__ x, int64_t x_ld, QDesc q,
-                                                        FastDiv fd_nbr, uint32_t nb, uint32_t* __restrict__ status) {
-  uint32_t bad = 0;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
-    const uint32_t r = fdiv(b, fd_nbr), kb = b - r * fd_nbr.d;
-    Blk16<DT> h0, h1;
-    ld_blk<DT>(x, (int64_t)r * x_ld + kb * 32, h0);
-    ld_blk<DT>(x, (int64_t)r * x_ld + kb * 32 + 16, h1);
-    const float alpha = fmaxf(blk_absmax<DT>(h0, bad), blk_absmax<DT>(h1, bad));
-    const uint8_t biased = e8m0_biased_ocp(alpha);
-    const float sf = exp2i_f32(127 - (int)biased);
-    float v[16];
-    uint32_t c0[2], c1[2];
-    blk_f32<DT>(h0, v);
-    enc16(v, sf, c0);
-    blk_f32<DT>(h1, v);
-    enc16(v, sf, c1);
-    *reinterpret_cast<uint4*>(q.codes + (int64_t)r * q.codes_ld + kb * 16) = make_uint4(c0[0], c0[1], c1[0], c1[1]);
-    store_scale(q, r, kb, biased);
-  }
-  if (bad) atomicOr(status, ST_NONFINITE);
 }
 
 // ---------------------------------------------------------------------------
@@ -354,6 +268,212 @@ __global__ void __launch_bounds__(256) k_quantize_mbs_s(const void* __restrict__
   }
   if (bad) atomicOr(status, ST_NONFINITE);
   if (ovf_any) atomicOr(status, ST_OVERFLOW);
+}
+
+// ---------------------------------------------------------------------------
+// Row-tiled streaming path (K1, K2 and K4 pass 2).  A CTA takes a tile of 256
+// consecutive 16-element units of one row (4096 elements); unit kb of the row
+// belongs to lane kb % 32, so loads and code stores are coalesced and all row /
+// tile index math is CTA-uniform.  G consecutive lanes share one scale (OCP32:
+// G = 2) or one MBS macro (G = macro/16, a power of two); SQ_UNROLL tiles are
+// in flight per thread.
+// ---------------------------------------------------------------------------
+constexpr int SQ_THREADS = 256;
+constexpr int SQ_UNROLL = 4;  // tiles per thread in flight
+constexpr int SQ_FOLD_LO = 27, SQ_FOLD_HI = 227;  // biased range where x*(f*SF) == RN(x*f)*SF for every code
+
+enum { SQ_OCP32 = 0, SQ_MX16 = 1, SQ_OAS = 2, SQ_MBS_S = 3 };
+
+__device__ __forceinline__ void store_scale_u(const QDesc& q, uint32_t r, uint32_t kbs, uint8_t s) {
+  if (q.scales) q.scales[(int64_t)r * q.scales_ld + kbs] = s;
+  if (q.scales_mma) q.scales_mma[sf_mma_offset(r, kbs, q.sf_kpad)] = s;
+}
+
+template <int DT, int VAR, int G>
+__device__ __forceinline__ void sq_unit(const Blk16<DT>& xb, bool active, const QDesc& q, uint32_t r, uint32_t kb,
+                                        uint32_t lane, const float* sig_tab, uint32_t& bad, uint32_t& ovf_any) {
+  float a = blk_absmax<DT>(xb, bad);
+  float v[16];
+  blk_f32<DT>(xb, v);
+  uint32_t codes[2];
+  if constexpr (VAR == SQ_MBS_S) {
+    // src/quantize.py:383-406: m8 from the macro max, y = RN(x*f), OAS on y
+    const float amac = G > 1 ? group_max(a, G) : a;
+    const uint8_t m8 = static_m8(amac);
+    const float f = mbs_factor(m8);
+    const float af = __fmul_rn(a, f);
+    const uint8_t biased = e8m0_biased_16(af, true);
+    if (active && !(af <= 3.402823466e38f)) ovf_any = 1u;
+    const float sf = exp2i_f32(127 - (int)biased);
+    if (__all_sync(0xffffffffu, biased >= SQ_FOLD_LO && biased <= SQ_FOLD_HI)) {
+      // f*SF is exact and RN(x*f)*SF == RN(x*(f*SF)) for every element that
+      // can reach a nonzero code (quantizer section)
+      enc16(v, __fmul_rn(f, sf), codes);
+    } else {
+      float y[16];
+#pragma unroll
+      for (int i = 0; i < 16; i += 2) fmul2(y[i], y[i + 1], v[i], v[i + 1], f);
+      enc16(y, sf, codes);
+    }
+    if (active) {
+      *reinterpret_cast<uint2*>(q.codes + (int64_t)r * q.codes_ld + kb * 8) = make_uint2(codes[0], codes[1]);
+      store_scale_u(q, r, kb, biased);
+      if ((lane & (G - 1)) == 0) {
+        const uint32_t mac = kb / G;
+        if (q.mant) q.mant[(int64_t)r * q.mant_ld + mac] = m8;
+        if (q.sig_t) q.sig_t[(int64_t)mac * q.sig_t_ld + r] = sig_tab[m8];
+      }
+    }
+  } else {
+    if constexpr (VAR == SQ_OCP32) a = group_max(a, 2);
+    const uint8_t biased = VAR == SQ_OCP32 ? e8m0_biased_ocp(a) : e8m0_biased_16(a, VAR == SQ_OAS);
+    enc16(v, exp2i_f32(127 - (int)biased), codes);
+    if (active) {
+      *reinterpret_cast<uint2*>(q.codes + (int64_t)r * q.codes_ld + kb * 8) = make_uint2(codes[0], codes[1]);
+      if (VAR != SQ_OCP32) store_scale_u(q, r, kb, biased);
+      else if ((lane & 1) == 0) store_scale_u(q, r, kb >> 1, biased);
+    }
+  }
+}
+
+template <int DT, int VAR, int G>
+__global__ void __launch_bounds__(SQ_THREADS) k_stream_quant(const void* __restrict__ x, int64_t x_ld, QDesc q,
+                                                             uint32_t nblk, uint32_t tpr, uint32_t ntiles,
+                                                             uint32_t* __restrict__ status) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  uint32_t bad = 0, ovf_any = 0;
+  // sigma = 1/(1+m8/256) for every m8 (IEEE f32 division, as the GEMM layout
+  // expects), one entry per thread, instead of a division per macro
+  __shared__ float sig_tab[256];
+  if constexpr (VAR == SQ_MBS_S) {
+    sig_tab[tid] = 1.0f / mbs_factor(tid);
+    __syncthreads();
+  }
+  for (uint32_t t0 = blockIdx.x; t0 < ntiles; t0 += SQ_UNROLL * gridDim.x) {
+    // all SQ_UNROLL tiles' loads first: a 4096 x 4096 tensor is in flight at once
+    Blk16<DT> xb[SQ_UNROLL];
+    uint32_t rr[SQ_UNROLL], kk[SQ_UNROLL];
+#pragma unroll
+    for (int u = 0; u < SQ_UNROLL; ++u) {
+      const uint32_t t = t0 + u * gridDim.x;
+      rr[u] = t / tpr;
+      kk[u] = (t - rr[u] * tpr) * SQ_THREADS + tid;
+      if (t < ntiles && kk[u] < nblk) ld_blk<DT>(x, (int64_t)rr[u] * x_ld + kk[u] * 16, xb[u]);
+      else zero_blk<DT>(xb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < SQ_UNROLL; ++u) {
+      const uint32_t t = t0 + u * gridDim.x;
+      if (t < ntiles) sq_unit<DT, VAR, G>(xb[u], kk[u] < nblk, q, rr[u], kk[u], lane, sig_tab, bad, ovf_any);
+    }
+  }
+  if (bad) atomicOr(status, ST_NONFINITE);
+  if (ovf_any) atomicOr(status, ST_OVERFLOW);
+}
+
+// K4 pass 1: |x| max of the whole tensor (uint ordering of non-negative
+// floats) and the non-finite check, same tiling, one atomic per warp.
+template <int DT>
+__global__ void __launch_bounds__(SQ_THREADS) k_stream_absmax(const void* __restrict__ x, int64_t x_ld,
+                                                              uint32_t nblk, uint32_t tpr, uint32_t ntiles,
+                                                              uint32_t* __restrict__ status) {
+  const uint32_t tid = threadIdx.x;
+  uint32_t bad = 0;
+  float m = 0.0f;
+  for (uint32_t t0 = blockIdx.x; t0 < ntiles; t0 += SQ_UNROLL * gridDim.x) {
+    Blk16<DT> xb[SQ_UNROLL];
+#pragma unroll
+    for (int u = 0; u < SQ_UNROLL; ++u) {
+      const uint32_t t = t0 + u * gridDim.x;
+      const uint32_t r = t / tpr, kb = (t - r * tpr) * SQ_THREADS + tid;
+      if (t < ntiles && kb < nblk) ld_blk<DT>(x, (int64_t)r * x_ld + kb * 16, xb[u]);
+      else zero_blk<DT>(xb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < SQ_UNROLL; ++u) m = fmaxf(m, blk_absmax<DT>(xb[u], bad));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((tid & 31) == 0) {
+    if (m > 0.0f) atomicMax(status + 1, __float_as_uint(m));
+    if (bad) atomicOr(status, ST_NONFINITE);
+  }
+}
+
+// K4 pass 2.  The element code is E2M1-RN of the f64 quotient x/(s_t*d)
+// (src/quantize.py:684-700).  The quotient is estimated in f32 (relative error
+// < 2^-21) and encoded at t*(1-2^-17), t and t*(1+2^-17); E2M1 rounding is
+// monotone, so when all three codes agree they equal the code of the exact
+// f64 quotient.  Only pairs that straddle a rounding boundary (or an
+// out-of-range denominator) take the f64 division.
+template <int DT>
+__device__ __forceinline__ void nvfp4_unit(const Blk16<DT>& xb, bool active, const QDesc& q, uint32_t r, uint32_t kb,
+                                           double st, double six_st, bool nz) {
+  uint32_t bad_unused = 0;
+  const float alpha = blk_absmax<DT>(xb, bad_unused);
+  const uint32_t sb = nz ? e4m3_code_f64((double)alpha / six_st) : 0u;
+  const double den = st * e4m3_decode(sb);
+  float v[16];
+  blk_f32<DT>(xb, v);
+  uint32_t packed[2] = {0u, 0u};
+  if (den > 0.0) {
+    const bool f32_ok = den > 1e-30 && den < 1e30;
+    const float inv = f32_ok ? __frcp_rn(__double2float_rn(den)) : 0.0f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = 8 * h + 2 * j;
+        float t0, t1, l0, l1, u0, u1;
+        fmul2(t0, t1, v[i], v[i + 1], inv);
+        fmul2(l0, l1, t0, t1, 0.99999237060546875f);   // 1 - 2^-17
+        fmul2(u0, u1, t0, t1, 1.00000762939453125f);   // 1 + 2^-17
+        uint32_t c = cvt_e2m1x2(t0, t1);
+        const uint32_t cl = cvt_e2m1x2(l0, l1), cu = cvt_e2m1x2(u0, u1);
+        if (!f32_ok || cl != c || cu != c)
+          c = e2m1_code_f64(__ddiv_rn((double)v[i], den)) | (e2m1_code_f64(__ddiv_rn((double)v[i + 1], den)) << 4);
+        word |= c << (8 * j);
+      }
+      packed[h] = fix_neg_zero(word);
+    }
+  }
+  if (active) {
+    *reinterpret_cast<uint2*>(q.codes + (int64_t)r * q.codes_ld + kb * 8) = make_uint2(packed[0], packed[1]);
+    store_scale_u(q, r, kb, (uint8_t)sb);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(SQ_THREADS) k_stream_nvfp4(const void* __restrict__ x, int64_t x_ld, QDesc q,
+                                                             uint32_t nblk, uint32_t tpr, uint32_t ntiles,
+                                                             const uint32_t* __restrict__ amax_bits) {
+  const float amax = __uint_as_float(*amax_bits);
+  const bool nz = amax > 0.0f;
+  const double st = nz ? (double)amax / 2688.0 : 1.0;
+  const double six_st = 6.0 * st;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && q.tensor_scale) *q.tensor_scale = st;
+  constexpr int NV_UNROLL = 2;  // (the f64 fallback path needs the registers)
+  const uint32_t tid = threadIdx.x;
+  for (uint32_t t0 = blockIdx.x; t0 < ntiles; t0 += NV_UNROLL * gridDim.x) {
+    Blk16<DT> xb[NV_UNROLL];
+    uint32_t rr[NV_UNROLL], kk[NV_UNROLL];
+#pragma unroll
+    for (int u = 0; u < NV_UNROLL; ++u) {
+      const uint32_t t = t0 + u * gridDim.x;
+      rr[u] = t / tpr;
+      kk[u] = (t - rr[u] * tpr) * SQ_THREADS + tid;
+      if (t < ntiles && kk[u] < nblk) ld_blk<DT>(x, (int64_t)rr[u] * x_ld + kk[u] * 16, xb[u]);
+      else zero_blk<DT>(xb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < NV_UNROLL; ++u) {
+      const uint32_t t = t0 + u * gridDim.x;
+      if (t < ntiles) nvfp4_unit<DT>(xb[u], kk[u] < nblk, q, rr[u], kk[u], st, six_st, nz);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -530,63 +650,6 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
 }
 
 // ---------------------------------------------------------------------------
-// K4: NVFP4.  Pass 1: |x| max over the tensor (uint ordering of non-negative
-// floats), non-finite check.  Pass 2: per-block E4M3 scale from the f64 ratio
-// and f64 element division (f32 division changes 1-2 codes per
-// 16.8M elements).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_absmax(const void* __restrict__ x, int dtype, int64_t x_ld, int64_t rows,
-                                                int64_t cols, uint32_t* __restrict__ status) {
-  const int64_t nbr = cols / 16, nb = rows * nbr;
-  float m = 0.0f;
-  uint32_t bad = 0;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = b / nbr, kb = b - r * nbr;
-    float v[16];
-    load_block<16>(x, dtype, r * x_ld + kb * 16, v);
-    bool fin;
-    m = fmaxf(m, block_absmax<16>(v, fin));
-    bad |= !fin;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (m > 0.0f) atomicMax(status + 1, __float_as_uint(m));
-    if (bad) atomicOr(status, ST_NONFINITE);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_quantize_nvfp4(const void* __restrict__ x, int dtype, int64_t x_ld, QDesc q,
-                                                        const uint32_t* __restrict__ amax_bits) {
-  const float amax = __uint_as_float(*amax_bits);
-  const double st = amax > 0.0f ? (double)amax / 2688.0 : 1.0;
-  const double six_st = 6.0 * st;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && q.tensor_scale) *q.tensor_scale = st;
-  const int64_t nbr = q.cols / 16, nb = q.rows * nbr;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = b / nbr, kb = b - r * nbr;
-    float v[16];
-    load_block<16>(x, dtype, r * x_ld + kb * 16, v);
-    bool fin;
-    const float alpha = block_absmax<16>(v, fin);
-    const uint32_t sb = amax > 0.0f ? e4m3_code_f64((double)alpha / six_st) : 0u;
-    const double den = st * e4m3_decode(sb);
-    uint32_t packed[2] = {0u, 0u};
-    if (den > 0.0) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const uint32_t c = e2m1_code_f64(__ddiv_rn((double)v[i], den));
-        packed[i >> 3] |= c << (4 * (i & 7));
-      }
-    }
-    store_codes<16>(q.codes + r * q.codes_ld + kb * 8, packed);
-    store_scale(q, r, kb, (uint8_t)sb);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // K5: dequantise to f32 (src/quantize.py:728-746).  Thread == block.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_dequantize(QDesc q, float* __restrict__ out, int64_t out_ld,
@@ -643,28 +706,28 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
   const int64_t nbr16 = cols / 16;
   if (rows * nbr16 >= (int64_t)1 << 31) return set_error(ERR_UNSUPPORTED, "tensor too large (>= 2^31 blocks)");
   const bool bf = dtype == DT_BF16;
+  // Row-tiled streaming grid (see k_stream_quant)
+  const uint32_t nblk = (uint32_t)nbr16;
+  const uint32_t tpr = (uint32_t)((nbr16 + SQ_THREADS - 1) / SQ_THREADS);
+  const int64_t ntiles64 = rows * (int64_t)tpr;
+  if (ntiles64 >= (int64_t)1 << 31) return set_error(ERR_UNSUPPORTED, "tensor too large");
+  const uint32_t ntiles = (uint32_t)ntiles64;
+  const int sq_grid = (int)std::min<int64_t>((ntiles + SQ_UNROLL - 1) / SQ_UNROLL, (int64_t)num_sms() * 8);
+#define SQ_LAUNCH(VAR, G)                                                                                        \
+  do {                                                                                                          \
+    if (bf) k_stream_quant<DT_BF16, VAR, G><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status); \
+    else k_stream_quant<DT_F32, VAR, G><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status);     \
+  } while (0)
   switch (q.variant) {
-    case OCP32: {
-      const uint32_t nb = (uint32_t)(rows * (cols / 32));
-      const FastDiv fd = make_fastdiv((uint32_t)(cols / 32));
-      if (bf) k_quantize_ocp32<DT_BF16><<<grid_for(nb, 256), 256, 0, st>>>(x, x_ld, q, fd, nb, status);
-      else k_quantize_ocp32<DT_F32><<<grid_for(nb, 256), 256, 0, st>>>(x, x_ld, q, fd, nb, status);
+    case OCP32:
+      SQ_LAUNCH(SQ_OCP32, 2);
       break;
-    }
     case MX16:
-    case MX16_OAS: {
-      const uint32_t nb = (uint32_t)(rows * nbr16);
-      const FastDiv fd = make_fastdiv((uint32_t)nbr16);
-      const int grid = grid_for((nb + 1) / 2, 256);
-      if (q.variant == MX16) {
-        if (bf) k_quantize_mx16<DT_BF16, false><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
-        else k_quantize_mx16<DT_F32, false><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
-      } else {
-        if (bf) k_quantize_mx16<DT_BF16, true><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
-        else k_quantize_mx16<DT_F32, true><<<grid, 256, 0, st>>>(x, x_ld, q, fd, nb, status);
-      }
+      SQ_LAUNCH(SQ_MX16, 1);
       break;
-    }
+    case MX16_OAS:
+      SQ_LAUNCH(SQ_OAS, 1);
+      break;
     case MBS_S:
     case MBS_D: {
       MacroGeom g;
@@ -673,7 +736,16 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       g.nmac = (cols + q.macro_size - 1) / q.macro_size;
       if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
       const int64_t ngroups = rows * g.nmac;
-      if (q.variant == MBS_S) {
+      if (q.variant == MBS_S && g.G * 16 == g.macro) {
+        switch (g.G) {  // power-of-two macro: G lanes per macro inside the row tile
+          case 1: SQ_LAUNCH(SQ_MBS_S, 1); break;
+          case 2: SQ_LAUNCH(SQ_MBS_S, 2); break;
+          case 4: SQ_LAUNCH(SQ_MBS_S, 4); break;
+          case 8: SQ_LAUNCH(SQ_MBS_S, 8); break;
+          case 16: SQ_LAUNCH(SQ_MBS_S, 16); break;
+          default: SQ_LAUNCH(SQ_MBS_S, 32); break;
+        }
+      } else if (q.variant == MBS_S) {
         const FastDiv fd = make_fastdiv((uint32_t)g.nmac);
         const int grid = grid_for(ngroups * g.G, 256);
         if (bf) k_quantize_mbs_s<DT_BF16><<<grid, 256, 0, st>>>(x, x_ld, q, g, fd, (uint32_t)ngroups, status);
@@ -695,8 +767,15 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       const int64_t nb = rows * (cols / 16);
       cudaError_t e = cudaMemsetAsync(status + 1, 0, sizeof(uint32_t), st);
       if (e != cudaSuccess) return set_cuda_error(e);
-      k_absmax<<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, rows, cols, status);
-      k_quantize_nvfp4<<<grid_for(nb, 256), 256, 0, st>>>(x, dtype, x_ld, q, status + 1);
+      (void)nb;
+      const int nv_grid = (int)std::min<int64_t>((ntiles + 1) / 2, (int64_t)num_sms() * 8);
+      if (bf) {
+        k_stream_absmax<DT_BF16><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, nblk, tpr, ntiles, status);
+        k_stream_nvfp4<DT_BF16><<<nv_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status + 1);
+      } else {
+        k_stream_absmax<DT_F32><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, nblk, tpr, ntiles, status);
+        k_stream_nvfp4<DT_F32><<<nv_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status + 1);
+      }
       break;
     }
     default:

@@ -218,3 +218,54 @@ def test_matmul_reference_exact():
     assert np.array_equal(M.matmul_reference(a, b).cpu().numpy(), O.matmul_ref(a, b))
     one = M.matmul_reference(np.array([[2.0, 3.0]], np.float32), np.array([[4.0, 5.0]], np.float32))
     assert float(one[0, 0]) == 23.0
+
+
+def test_nvfp4_rounding_boundaries_match_oracle():
+    """NVFP4 pass 2 estimates x/(s_t*d) in f32 and falls back to the f64
+    division only near an E2M1 rounding boundary: elements exactly on every
+    midpoint (ties to the even index) and one f32 ulp either side, for
+    denominators 1 and 0.5 (s_t = 1 from a global max of 2688)."""
+    mids = np.array([0.25, 0.75, 1.25, 1.75, 2.5, 3.5, 5.0], np.float32)
+    vals = np.concatenate([mids, np.nextafter(mids, np.float32(0)), np.nextafter(mids, np.float32(10))])
+    vals = np.concatenate([vals, -vals])
+    blocks = []
+    for scale in (1.0, 0.5):
+        v = (vals * scale).astype(np.float32)
+        for i in range(0, len(v), 15):
+            blk = np.zeros(16, np.float32)
+            chunk = v[i:i + 15]
+            blk[:len(chunk)] = chunk
+            blk[15] = 6.0 * scale  # block max -> E4M3 d = scale
+            blocks.append(blk)
+    row = np.concatenate(blocks)
+    t = np.zeros((3, row.size), np.float32)
+    t[0], t[1] = row, -row
+    t[2, 0] = 2688.0  # global |max| -> s_t = 1
+    q = M.quantize_tensor(t, M.SchemeConfig(M.Variant.NVFP4))
+    o = O.quantize(t, "nvfp4")
+    assert float(q.tensor_scale) == o.tensor_scale == 1.0
+    assert np.array_equal(_np(q.codes), o.codes)
+    assert np.array_equal(_np(q.e4m3_scales), o.e4m3_scales)
+
+
+@pytest.mark.parametrize("variant", ["ocp32", "mx16", "mx16_oas", "mbs_s", "nvfp4"])
+def test_streaming_quantizer_ragged_rows_match_oracle(variant):
+    """Row-tiled streaming kernels: rows longer than one 4096-element tile and
+    not a multiple of it, tiny (f32-subnormal) and huge blocks in one row
+    (the MBS-S folded / unfolded scaling paths), macro 64 and 256 for MBS-S."""
+    rng = np.random.Generator(np.random.PCG64(77))
+    t = rng.standard_t(4, (5, 4096 + 1024 + 96)).astype(np.float32)
+    t[1, :256] *= np.float32(1e-40)
+    t[2, 512:640] *= np.float32(1e30)
+    t[3, 1000:1100] = 0.0
+    macros = (64, 128, 256) if variant == "mbs_s" else (128,)
+    for mac in macros:
+        if variant == "ocp32" and t.shape[1] % 32:
+            continue
+        q = M.quantize_tensor(t, M.SchemeConfig(M.Variant(variant), macro_size=mac))
+        o = O.quantize(t, variant, macro_size=mac)
+        assert np.array_equal(_np(q.codes), o.codes), (variant, mac)
+        sc = _np(q.block_scales) if q.block_scales is not None else _np(q.e4m3_scales)
+        assert np.array_equal(sc, o.block_scales if o.block_scales is not None else o.e4m3_scales)
+        if o.mbs_mantissas is not None:
+            assert np.array_equal(_np(q.mbs_mantissas), o.mbs_mantissas)
