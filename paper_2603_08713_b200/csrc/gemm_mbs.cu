@@ -51,6 +51,11 @@ constexpr int THREADS = 20 * 32;
 constexpr int ATOM = 512;                   // SF atom: 128 rows x 4 blocks of 16
 constexpr int STAGE_A = BM * KSTAGE / 2;    // 16 KB of A codes per stage
 constexpr int SFA_BYTES = 4 * ATOM;         // 4 k-steps
+// Scale factors reach TMEM by tcgen05.cp issued from the MMA warp (in order
+// with the MMAs, ~64 tensor-pipe cycles per atom, tools/microbench_cp.cu) --
+// the tensor pipe has the slack, the epilogue warps do not -- instead of
+// tcgen05.st from the epilogue warps (false).
+constexpr bool SF_CP = true;
 
 // Tile shape (BN output columns, NB TMEM partial buffers).  The product path
 // is BN=192, NB=2 (DESIGN.md section 3 lists the measured alternatives).
@@ -77,7 +82,7 @@ struct MbsCfg {
   static constexpr int COL_SF0 = (NB * BN + 63) / 64 * 64;
   static constexpr int SF_STRIDE = 64;
   // 16*32*EPI + 4*32*CTRL must fit the 96 x 640 registers allocated at launch
-  static constexpr bool SETMAXNREG = COLS > 32;
+  static constexpr bool SETMAXNREG = COLS > 32 || NB >= 3;  // NB >= 3 keeps two partials in registers
   static constexpr int EPI_REGS = 112, CTRL_REGS = 32;
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(OFF_B % 1024 == 0 && STAGE_B % 1024 == 0 && (BN / 2) * 128 % 1024 == 0, "128B-swizzle alignment");
@@ -135,6 +140,10 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
+}
+__device__ __forceinline__ void sf_cp_e(uint32_t tmem_col, uint32_t saddr) {
+  const uint64_t d = smem_desc(saddr, 0, 128, 0);  // 32 rows x 16 B, 8-row core matrices 128 B apart
+  asm volatile(MXQ_ELECT "tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;\n\t}" ::"r"(tmem_col), "l"(d) : "memory");
 }
 // Start a 16-column TMEM load without waiting (the caller waits once for all).
 __device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, float* v) {
@@ -291,12 +300,27 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (; ks < kend; ++ks) {
             const uint32_t j = (uint32_t)ks & 3u;
             if (j == 0) {
-              mbar_wait_a(a_sfready + (g & (NSFB - 1)) * 8, (g / NSFB) & 1u);
-              trace_at(p, q, 10);
-              tc_fence_after();
+              sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
+              if constexpr (SF_CP) {
+                mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
+                trace_at(p, q, 10);
+                tc_fence_after();
+                // this stage's SF atoms -> SF buffer g % 2 (the buffer's previous
+                // readers, stage g-2's MMAs, precede these copies in the pipe)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  sf_cp_e(sfa_col + 4 * jj, a_smem + OFF_SFA + st * SFA_BYTES + jj * ATOM);
+#pragma unroll
+                  for (int r = 0; r < NRB; ++r)
+                    sf_cp_e(sfa_col + 16 + 4 * NRB * jj + 4 * r, a_smem + OFF_SFB + st * SFB_BYTES + r * 4 * ATOM + jj * ATOM);
+                }
+              } else {
+                mbar_wait_a(a_sfready + (g & (NSFB - 1)) * 8, (g / NSFB) & 1u);
+                trace_at(p, q, 10);
+                tc_fence_after();
+              }
               adesc = operand_desc(a_smem + OFF_A + st * STAGE_A);
               bdesc = operand_desc(a_smem + OFF_B + st * STAGE_B);
-              sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
             }
             mma_bs_e<false>(dcol, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), p.idesc, ks > kbeg ? 1u : 0u,
                             sfa_col + 4 * j, sfa_col + 16 + 4 * NRB * j + sfb_shift);
@@ -359,7 +383,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     auto nx_advance = [&]() {
       if (++nx_c == n_chunks) { nx_c = 0; ++nx_t; }
     };
-    if (total_chunks > 0) {
+    if (!SF_CP && total_chunks > 0) {
       for (int i = 0; i < NB && i < total_chunks; ++i) {
         write_sf_upto(nx_stage());
         nx_advance();
@@ -378,7 +402,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // chunk ql is complete, so every MMA of the stages before it is too: the
       // SF buffer of chunk ql+NB's stage can be overwritten now (before the
       // release below lets chunk ql+NB's MMAs start; they wait for these).
-      if ((int)ql + NB < total_chunks) {
+      if (!SF_CP && (int)ql + NB < total_chunks) {
         write_sf_upto(nx_stage());
         nx_advance();
       }
@@ -425,12 +449,32 @@ __global__ void __launch_bounds__(THREADS, 1)
       float acc[COLS];
 #pragma unroll
       for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
+      if constexpr (NB >= 3) {
+        // two register sets: the TMEM loads of chunk c+1 are in flight while
+        // chunk c is folded (the MMA runs NB-1 chunks ahead, so they are ready)
+        float pa[COLS], pb[COLS];
+        start_load(pa);
+        finish_load(pa);
+        int c = 0;
 #pragma unroll 1
-      for (int c = 0; c < n_chunks; ++c) {
-        float v[COLS];
-        start_load(v);
-        finish_load(v);
-        compute(acc, v);
+        while (true) {
+          if (c + 1 < n_chunks) start_load(pb);
+          compute(acc, pa);
+          if (++c == n_chunks) break;
+          finish_load(pb);
+          if (c + 1 < n_chunks) start_load(pa);
+          compute(acc, pb);
+          if (++c == n_chunks) break;
+          finish_load(pa);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < n_chunks; ++c) {
+          float v[COLS];
+          start_load(v);
+          finish_load(v);
+          compute(acc, v);
+        }
       }
       // store the tile row (masked to M x N)
       if (row < p.M) {
@@ -550,6 +594,15 @@ bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
 }
 
 int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
+  static int shape = -1;  // development A/B: MXQ_GEMM_MBS_BN=128 selects the 128x128, three-buffer shape
+  if (shape < 0) {
+    const char* d = getenv("MXQ_GEMM_MBS_BN");
+    shape = (d && atoi(d) == 128) ? 128 : 192;
+  }
+  if (shape == 128) {
+    if (c_dtype == MXQ_BF16) return mbs::launch<128, 3, true, 2>(a, b, c, ldc, st);
+    return mbs::launch<128, 3, false, 2>(a, b, c, ldc, st);
+  }
   if (c_dtype == MXQ_BF16) return mbs::launch<192, 2, true, 2>(a, b, c, ldc, st);
   return mbs::launch<192, 2, false, 2>(a, b, c, ldc, st);
 }
