@@ -1,5 +1,5 @@
 """The bench's four Llama-3-8B MBS-H layer GEMMs (M=4096), each launched twice,
-for `ncu --set full -k regex:k_gemm_tc --launch-skip 4 --launch-count 4`:
+for `ncu --set full -k regex:k_gemm --launch-skip 4 --launch-count 4`:
 the second round is what gets captured (warm TMA descriptors, weights in HBM).
 Writes nothing; profiles/gemm_traffic.json is assembled from the ncu report."""
 import os, sys
