@@ -138,8 +138,9 @@ def run_ours(args):
         acts.append(torch.where(hit, x * 100.0, x).to(bf16))
     gw = torch.Generator(device=dev).manual_seed(4321 + rank)
     wdense, bounds = [], []
+    cols = args.mode == "columns" and world > 1  # tensor-parallel column shards + all_gather
     for _, n, k in LAYERS:
-        lo, hi = P.shard_bounds(n, world, rank)
+        lo, hi = P.shard_bounds(n, world, rank) if cols else (0, n)
         bounds.append((lo, hi))
         wdense.append((torch.randn(hi - lo, k, device=dev, generator=gw) * 0.02).to(bf16))
 
@@ -154,9 +155,12 @@ def run_ours(args):
     outs = [torch.empty(M_TOK, hi - lo, device=dev, dtype=bf16) for lo, hi in bounds]
     gathered = [torch.empty(world * M_TOK, max(P.shard_bounds(n, world, r)[1] - P.shard_bounds(n, world, r)[0]
                                                for r in range(world)), device=dev, dtype=bf16)
-                if world > 1 else None for _, n, _ in LAYERS]
+                if cols else None for _, n, _ in LAYERS]
     n_local_frac = sum(2.0 * M_TOK * (hi - lo) * k for (lo, hi), (_, _, k) in zip(bounds, LAYERS))
-    step_flops_global = flops_per_step()
+    # replicas (default): every rank runs the whole step on its own M tokens,
+    # no data-path collective, weak scaling; columns: one step split by output
+    # column across ranks plus the bf16 all_gather (config 4's pattern)
+    step_flops_global = flops_per_step() * (1 if cols else world)
 
     def step(arm, gemm_events=None):
         av, _ = arms[arm]
@@ -167,7 +171,7 @@ def run_ours(args):
             M.matmul_quantized(aq, weights[arm][li], out=outs[li], out_dtype=bf16, check=False)
             if gemm_events is not None:
                 gemm_events[li][1].record()
-            if world > 1:
+            if cols:
                 send = outs[li]
                 if send.shape[1] != gathered[li].shape[1]:
                     pad = torch.zeros(M_TOK, gathered[li].shape[1], device=dev, dtype=bf16)
@@ -184,7 +188,7 @@ def run_ours(args):
 
     def capture(arm):
         """The whole step (4 x quantize + GEMM [+ all_gather]) as one CUDA graph."""
-        if world > 1:
+        if cols:
             return None  # NCCL collectives are replayed eagerly
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
@@ -242,7 +246,7 @@ def run_ours(args):
                 "ms_per_step": ms,
                 "tflops_step": step_flops_global / (ms * 1e-3) / 1e12,
                 "gemm_ms": gemm_ms,
-                "gemm_tflops": n_local_frac / (gemm_ms * 1e-3) / 1e12 * world,
+                "gemm_tflops": n_local_frac / (gemm_ms * 1e-3) / 1e12 * world,  # all ranks' GEMM work / per-rank time
                 "gemm_ms_per_layer": {name: t for (name, _, _), t in zip(LAYERS, gl)},
             }
     head = results["mbs_h"]
@@ -304,36 +308,39 @@ def run_ours(args):
                          "equals_reference": rep.qsnr_db == ref["qsnr_db"] and fl == ref["flush"]}
         out["qsnr"] = qs
 
-        # ---- e2e: public API, pinned host activations in, bf16 out ---------
-        if world == 1:
-            host_in = [a.cpu().pin_memory() for a in acts]
-            host_out = [torch.empty(o.shape, dtype=bf16).pin_memory() for o in outs]
-            cfg_a = M.SchemeConfig(V.MBS_S)
+    # ---- e2e: public API, pinned host activations in, bf16 out -------------
+    # every rank (replicas) runs its own step from its own pinned host buffers;
+    # the time is the max over ranks
+    e2e = None
+    if not cols:
+        host_in = [a.cpu().pin_memory() for a in acts]
+        host_out = [torch.empty(o.shape, dtype=bf16).pin_memory() for o in outs]
+        cfg_a = M.SchemeConfig(V.MBS_S)
 
-            def e2e_step():
-                for li in range(len(LAYERS)):
-                    aq = M.quantize_tensor(host_in[li], cfg_a)      # H2D + quantize (+ status check)
-                    c = M.matmul_quantized(aq, weights["mbs_h"][li], out_dtype=bf16)
-                    host_out[li].copy_(c, non_blocking=True)        # D2H of the product
-                torch.cuda.synchronize()
-
-            for _ in range(max(2, W // 2)):
-                e2e_step()
-            ke = max(3, K // 2)
-            t0 = time.perf_counter()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(ke):
-                e2e_step()
-            e1.record()
+        def e2e_step():
+            for li in range(len(LAYERS)):
+                aq = M.quantize_tensor(host_in[li], cfg_a)      # H2D + quantize (+ status check)
+                c = M.matmul_quantized(aq, weights["mbs_h"][li], out_dtype=bf16)
+                host_out[li].copy_(c, non_blocking=True)        # D2H of the product
             torch.cuda.synchronize()
-            ms_e2e = e0.elapsed_time(e1) / ke
-            out["e2e"] = {"value": step_flops_global / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
-                          "h2d_bytes_per_step": int(sum(a.numel() * 2 for a in acts)),
-                          "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)),
-                          "ms_per_step": ms_e2e, "wall_ms_per_step": (time.perf_counter() - t0) * 1e3 / ke}
-        else:
-            out["e2e"] = None
+
+        for _ in range(max(2, W // 2)):
+            e2e_step()
+        ke = max(3, K // 2)
+        barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms_e2e = P.max_over_ranks(e0.elapsed_time(e1) / ke, device=dev)
+        wall = P.max_over_ranks((time.perf_counter() - t0) * 1e3 / ke, device=dev)
+        e2e = {"value": step_flops_global / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": int(sum(a.numel() * 2 for a in acts)) * world,
+               "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)) * world,
+               "ms_per_step": ms_e2e, "wall_ms_per_step": wall}
     if world > 1:
         dist.barrier(device_ids=[local])
 
@@ -385,10 +392,12 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(head["tflops_step"], 2), "unit": "TFLOP/s", "n_gpus": world,
         "steps": K, "warmup": W, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
+        "scaling": "strong" if cols else "weak", "vs_baseline": None,
+        "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
         "data": "synthetic (activations N(0,1) with 1% x100 outliers; random-init N(0,0.02) weights)",
-        "config": {"workload": WORKLOAD, "global_batch": M_TOK, "seq_len": None,
-                   "parallelism": f"column-shard x{world}" if world > 1 else "single",
+        "config": {"workload": WORKLOAD, "global_batch": M_TOK * (1 if cols else world), "seq_len": None,
+                   "parallelism": (f"column-shard x{world} + all_gather" if cols else
+                                   f"replicas x{world} (token-parallel, no collective)") if world > 1 else "single",
                    "l2": "inputs larger than L2 (218 MB bf16 activations + 121 MB fp4 weights per step)"},
         "gemm_only_tflops": round(head["gemm_tflops"], 2),
         "arms": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
@@ -401,7 +410,7 @@ def run_ours(args):
         "qsnr_config1": out["qsnr"],
         "roofline": roofline,
         "cpu_baseline": cpu,
-        "e2e": out["e2e"],
+        "e2e": e2e,
         "gpu_launches": 8 * K,
         "clocks": clk,
     }
@@ -503,6 +512,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--mode", default="replicas", choices=("replicas", "columns"),
+                    help="N>1: independent replicas on their own tokens (weak) or column shards + all_gather (strong)")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-wrows", type=int, default=2048)

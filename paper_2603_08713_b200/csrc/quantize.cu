@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(256) k_quantize_mbs_s(const void* __restrict__
 // in flight per thread.
 // ---------------------------------------------------------------------------
 constexpr int SQ_THREADS = 256;
-constexpr int SQ_UNROLL = 4;  // tiles per thread in flight
+#ifndef MXQ_SQ_UNROLL
+#define MXQ_SQ_UNROLL 4
+#endif
+constexpr int SQ_UNROLL = MXQ_SQ_UNROLL;  // tiles per thread in flight
 constexpr int SQ_FOLD_LO = 27, SQ_FOLD_HI = 227;  // biased range where x*(f*SF) == RN(x*f)*SF for every code
 
 enum { SQ_OCP32 = 0, SQ_MX16 = 1, SQ_OAS = 2, SQ_MBS_S = 3 };

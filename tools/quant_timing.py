@@ -9,8 +9,9 @@ import paper_2603_08713_b200 as M
 
 V = M.Variant
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+ncol = int(sys.argv[2]) if len(sys.argv) > 2 else n
 g = torch.Generator(device="cuda").manual_seed(0)
-xs = [torch.randn(n, n, device="cuda", generator=g).to(torch.bfloat16) for _ in range(8)]
+xs = [torch.randn(n, ncol, device="cuda", generator=g).to(torch.bfloat16) for _ in range(8)]
 for v, bpe in ((V.OCP32, 2.53125), (V.MX16, 2.5625), (V.MX16_OAS, 2.5625), (V.MBS_S, 2.5703125), (V.NVFP4, 2.5625)):
     cfg = M.SchemeConfig(v)
     for x in xs:
@@ -29,4 +30,4 @@ for v, bpe in ((V.OCP32, 2.53125), (V.MX16, 2.5625), (V.MX16_OAS, 2.5625), (V.MB
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    print(f"{v.value:9s} {ms*1e3:7.2f} us  {n*n*bpe/ms/1e6:7.0f} GB/s (HBM-cold inputs)", flush=True)
+    print(f"{v.value:9s} {n}x{ncol} {ms*1e3:7.2f} us  {n*ncol*bpe/ms/1e6:7.0f} GB/s (HBM-cold inputs)", flush=True)
