@@ -45,9 +45,6 @@ using namespace tc;
 constexpr int BM = 128;
 constexpr int KSTAGE = 256, KSTEP = 64;     // K elements per pipeline stage / per MMA
 constexpr int NSFB = 2, NSIG = 8;
-constexpr int EPIW = 16;                    // epilogue warps (4 per TMEM lane quadrant)
-constexpr int W_TMA = 16, W_MMA = 17;       // control warpgroup: warps 16..19
-constexpr int THREADS = 20 * 32;
 constexpr int ATOM = 512;                   // SF atom: 128 rows x 4 blocks of 16
 constexpr int STAGE_A = BM * KSTAGE / 2;    // 16 KB of A codes per stage
 constexpr int SFA_BYTES = 4 * ATOM;         // 4 k-steps
@@ -59,10 +56,13 @@ constexpr bool SF_CP = true;
 
 // Tile shape (BN output columns, NB TMEM partial buffers).  The product path
 // is BN=192, NB=2 (DESIGN.md section 3 lists the measured alternatives).
-template <int BN_, int NB_>
+template <int BN_, int NB_, int EPIW_>
 struct MbsCfg {
   static constexpr int BN = BN_, NB = NB_;
-  static constexpr int COLS = BN / 4;                   // output columns per epilogue thread
+  static constexpr int EPIW = EPIW_;                    // epilogue warps (EPIW/4 per TMEM lane quadrant)
+  static constexpr int W_TMA = EPIW, W_MMA = EPIW + 1;  // control warpgroup after them
+  static constexpr int THREADS = (EPIW + 4) * 32;
+  static constexpr int COLS = BN / (EPIW / 4);          // output columns per epilogue thread
   static constexpr int NRB = BN / 128 + (BN % 128 ? 1 : 0);  // 128-row SF atoms a tile can touch
   static constexpr int STAGES = BN > 128 ? 4 : 5;
   static constexpr int STAGE_B = BN * KSTAGE / 2;
@@ -81,9 +81,13 @@ struct MbsCfg {
   // an SF buffer: SFA of k-step j at +4j, SFB (NRB 128-row atoms) at +16+4*NRB*j.
   static constexpr int COL_SF0 = (NB * BN + 63) / 64 * 64;
   static constexpr int SF_STRIDE = 64;
-  // 16*32*EPI + 4*32*CTRL must fit the 96 x 640 registers allocated at launch
+  // EPIW*32*EPI + 4*32*CTRL must fit the registers allocated at launch
+  // (ptxas' per-thread count x THREADS: 96 x 640 for 16 epilogue warps,
+  // 168 x 384 for 8) -- setmaxnreg.inc blocks forever otherwise
   static constexpr bool SETMAXNREG = COLS > 32 || NB >= 3;  // NB >= 3 keeps two partials in registers
-  static constexpr int EPI_REGS = 112, CTRL_REGS = 32;
+  static constexpr int EPI_REGS = EPIW == 16 ? 112 : 208, CTRL_REGS = EPIW == 16 ? 32 : 48;
+  static_assert(EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= (EPIW == 16 ? 96 * 640 : 168 * 384), "register pool");
+  static_assert(SF_CP || EPIW == 16, "epilogue SF writing assigns one k-step per column group");
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(OFF_B % 1024 == 0 && STAGE_B % 1024 == 0 && (BN / 2) * 128 % 1024 == 0, "128B-swizzle alignment");
   static_assert(COL_SF0 + NSFB * SF_STRIDE <= 512, "TMEM budget");
@@ -167,10 +171,11 @@ __device__ __forceinline__ void reg_fence(float* v) {
                  "+f"(v[i + 6]), "+f"(v[i + 7]));
 }
 
-template <int BN_, int NB_, bool OUT_BF16, int CL>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL>
+__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
     k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
-  using C = MbsCfg<BN_, NB_>;
+  using C = MbsCfg<BN_, NB_, EPIW_>;
+  constexpr int EPIW = C::EPIW, W_TMA = C::W_TMA, W_MMA = C::W_MMA;
   constexpr int BN = C::BN, NB = C::NB, STAGES = C::STAGES, COLS = C::COLS, NRB = C::NRB;
   constexpr int STAGE_B = C::STAGE_B, SFB_BYTES = C::SFB_BYTES, SIG_SLOT = C::SIG_SLOT;
   constexpr int OFF_A = C::OFF_A, OFF_B = C::OFF_B, OFF_SFA = C::OFF_SFA, OFF_SFB = C::OFF_SFB;
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // ===================== epilogue (warps 0..15) =====================
     if constexpr (C::SETMAXNREG) setmaxnreg_inc<C::EPI_REGS>();
-    const int quad = warp & 3, grp = warp >> 2;
+    const int quad = warp & 3, grp = warp >> 2;  // TMEM lane quadrant, column group
     const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
     const uint32_t t_ld = t_lane + grp * COLS;
     const int row_in_tile = quad * 32 + lane;
@@ -520,11 +525,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
-template <int BN, int NB, bool OUT_BF16, int CL>
+template <int BN, int NB, int EPIW, bool OUT_BF16, int CL>
 static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStream_t st) {
-  using C = MbsCfg<BN, NB>;
+  using C = MbsCfg<BN, NB, EPIW>;
   constexpr int SMEM = C::SMEM;
-  auto kern = k_gemm_mbs<BN, NB, OUT_BF16, CL>;
+  auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -565,7 +570,7 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStre
   if (units < clusters) clusters = units;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CL);
-  cfg.blockDim = dim3(THREADS);
+  cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -594,17 +599,15 @@ bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
 }
 
 int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
-  static int shape = -1;  // development A/B: MXQ_GEMM_MBS_BN=128 selects the 128x128, three-buffer shape
+  static int shape = -1;  // development A/B (MXQ_GEMM_MBS_SHAPE): 1 = 16 warps x 48 cols, 2 = 8 warps x 96, 3 = 128x128 NB=3
   if (shape < 0) {
-    const char* d = getenv("MXQ_GEMM_MBS_BN");
-    shape = (d && atoi(d) == 128) ? 128 : 192;
+    const char* d = getenv("MXQ_GEMM_MBS_SHAPE");
+    shape = d ? atoi(d) : 1;
   }
-  if (shape == 128) {
-    if (c_dtype == MXQ_BF16) return mbs::launch<128, 3, true, 2>(a, b, c, ldc, st);
-    return mbs::launch<128, 3, false, 2>(a, b, c, ldc, st);
-  }
-  if (c_dtype == MXQ_BF16) return mbs::launch<192, 2, true, 2>(a, b, c, ldc, st);
-  return mbs::launch<192, 2, false, 2>(a, b, c, ldc, st);
+  const bool bf = c_dtype == MXQ_BF16;
+  if (shape == 2) return bf ? mbs::launch<192, 2, 8, true, 2>(a, b, c, ldc, st) : mbs::launch<192, 2, 8, false, 2>(a, b, c, ldc, st);
+  if (shape == 3) return bf ? mbs::launch<128, 3, 16, true, 2>(a, b, c, ldc, st) : mbs::launch<128, 3, 16, false, 2>(a, b, c, ldc, st);
+  return bf ? mbs::launch<192, 2, 16, true, 2>(a, b, c, ldc, st) : mbs::launch<192, 2, 16, false, 2>(a, b, c, ldc, st);
 }
 
 }  // namespace mxq
