@@ -70,7 +70,7 @@ class Clocks:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -514,7 +514,7 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": env_int("WORLD_SIZE", 1),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "fp64 reference arithmetic (numpy)",
+        "scaling": "weak", "vs_baseline": None, "dtype": "fp64 reference arithmetic (numpy)",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": WORKLOAD, "global_batch": M_TOK, "seq_len": None, "parallelism": "host cores"},
         "cpu_baseline": {"value": round(val, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
