@@ -53,6 +53,7 @@ struct Params {
   const uint8_t* sfa;   // scale-factor atoms, [M/128][kgroups][512]
   const uint8_t* sfb;
   int64_t sfa_kg, sfb_kg;  // 4-block groups per 128-row block (sf_kpad / 4)
+  int sfb_rb;              // allocated 128-row SF blocks of B
   const float* sga;     // MBS sigma, transposed (n_macros, ld) f32, or null (sigma = 1)
   const float* sgb;
   int64_t sga_ld, sgb_ld;
@@ -129,7 +130,10 @@ struct Cfg {
   static constexpr int STAGE_BYTES_B = BN * KSTAGE / 2;
   static constexpr int SF_ATOMS_PER_STAGE = SF32 ? 2 : 4;  // 512-B atoms per 128 rows per stage
   static constexpr int SFA_BYTES = SF_ATOMS_PER_STAGE * 512;
-  static constexpr int SFB_BYTES = SF_ATOMS_PER_STAGE * 512 * (BN / 128);
+  // 128-row SF atoms a B tile can touch (a 192-column tile at an odd position
+  // starts 64 rows into an atom, so it spans two)
+  static constexpr int NRB = BN / 128 + (BN % 128 ? 1 : 0);
+  static constexpr int SFB_BYTES = SF_ATOMS_PER_STAGE * 512 * NRB;
   static constexpr int OFF_A = 0;
   static constexpr int OFF_B = OFF_A + STAGES * STAGE_BYTES_A;
   static constexpr int OFF_SFA = OFF_B + STAGES * STAGE_BYTES_B;
@@ -141,8 +145,12 @@ struct Cfg {
   static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
   // TMEM scale-factor buffers: as many as fit beside the accumulators (<= 4),
   // so the SF writers run up to NSFB-1 stages ahead of the MMAs.
-  static constexpr int SF_COLS_STAGE = SF_ATOMS_PER_STAGE * 4 * (1 + BN / 128);
-  static constexpr int NSFB_FIT = (512 - NB * BN) / SF_COLS_STAGE;
+  static constexpr int SF_COLS_STAGE = SF_ATOMS_PER_STAGE * 4 * (1 + NRB);
+  // SF buffers 64-column aligned when two of them still fit (misaligned SF
+  // addresses slow the MMA, tools/microbench_mma3.cu)
+  static constexpr int SF_STRIDE = (512 - NB * BN) / ((SF_COLS_STAGE + 63) / 64 * 64) >= 2
+                                       ? (SF_COLS_STAGE + 63) / 64 * 64 : SF_COLS_STAGE;
+  static constexpr int NSFB_FIT = (512 - NB * BN) / SF_STRIDE;
   static constexpr int NSFB = NSFB_FIT >= 4 ? 4 : (NSFB_FIT >= 2 ? 2 : 1);
   // When every smem stage has its own SF buffer, the SF writers reuse the
   // stage's `empty` barrier (MMA completion) instead of a separate commit.
@@ -152,9 +160,9 @@ struct Cfg {
   static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
   // TMEM columns: NB accumulators of BN columns, then 2 parity sets of SF.
   static constexpr int SFA_COLS = SF_ATOMS_PER_STAGE * 4;
-  static constexpr int SFB_COLS = SF_ATOMS_PER_STAGE * 4 * (BN / 128);
+  static constexpr int SFB_COLS = SF_ATOMS_PER_STAGE * 4 * NRB;
   static constexpr int COL_SF = NB * BN;
-  static constexpr int TMEM_COLS_USED = COL_SF + NSFB * (SFA_COLS + SFB_COLS);
+  static constexpr int TMEM_COLS_USED = COL_SF + NSFB * SF_STRIDE;
   static constexpr int TMEM_COLS = 512;
   // 8 epilogue warps: 2 per TMEM lane quadrant, BN/2 columns each.
   static constexpr int EPIW = MBS ? 8 : 16;  // MBS: 64 columns per thread (issue-bound epilogue)
@@ -260,6 +268,8 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const int m0 = mb * BM, n0 = nb * BN;
       const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * 512;
       const uint8_t* sb = p.sfb + (int64_t)(n0 / 128) * p.sfb_kg * 512;
+      const int nrb = (n0 / 128 + C::NRB <= p.sfb_rb) ? C::NRB : p.sfb_rb - n0 / 128;
+      const uint32_t tx = C::TX_BYTES - (C::NRB - nrb) * C::SFA_BYTES;
       for (int s = 0; s < n_stages; ++s) {
         const uint32_t fb = a_full + stage * 8;
         mbar_wait_sleep(a_empty + stage * 8, phase ^ 1);
@@ -268,7 +278,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           continue;
         }
-        expect_tx_e(fb, C::TX_BYTES);
+        expect_tx_e(fb, tx);
         tma_load_2d_e(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
         if constexpr (CL == 1) {
           tma_load_2d_e(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B, &tmB, fb, s * (KSTAGE / 2), n0);
@@ -277,8 +287,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
                            s * (KSTAGE / 2), n0 + (int)crank * (BN / CL), (uint16_t)((1u << CL) - 1));
         }
         bulk_load_e(a_smem + C::OFF_SFA + stage * C::SFA_BYTES, sa + (int64_t)s * C::SFA_BYTES, C::SFA_BYTES, fb);
-#pragma unroll
-        for (int rb = 0; rb < BN / 128; ++rb)
+        for (int rb = 0; rb < nrb; ++rb)
           bulk_load_e(a_smem + C::OFF_SFB + stage * C::SFB_BYTES + rb * C::SFA_BYTES,
                       sb + ((int64_t)rb * p.sfb_kg * 512 + (int64_t)s * C::SFA_BYTES), C::SFA_BYTES, fb);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -295,16 +304,19 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const int chunk_len = MBS ? p.macro_steps : (1 << 30);
       int s = 0, kstep = 0, in_chunk = 0, tchunk = 0;
       bool open = false;
+      int unit = unit0;
       for (int g = 0; g < total; ++g) {
         const uint32_t par = (uint32_t)g % C::NSFB;
+        // a 192-column tile at an odd position starts 64 rows (2 SF columns) into its first atom
+        const uint32_t sfb_shift = ((unit / groups_m) * BN % 128) ? 2u : 0u;
         // sf_ready implies full: the SF writers waited for this stage's TMA
         // transaction (A, B and scale bytes) before writing the SF to TMEM.
         trace_at(p, tchunk, 4);
         mbar_wait_a(a_sf_ready + par * 8, ((uint32_t)g / C::NSFB) & 1u);
         trace_at(p, tchunk, 5);
         tc_fence_after();
-        const uint32_t sfa_col = tmem + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
-        const uint32_t sfb_col = sfa_col + C::SFA_COLS;
+        const uint32_t sfa_col = tmem + C::COL_SF + par * C::SF_STRIDE;
+        const uint32_t sfb_col = sfa_col + C::SFA_COLS + sfb_shift;
         const uint64_t adesc = operand_desc(a_smem + C::OFF_A + stage * STAGE_BYTES_A);
         const uint64_t bdesc = operand_desc(a_smem + C::OFF_B + stage * C::STAGE_BYTES_B);
 #pragma unroll
@@ -331,7 +343,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
             }
             // +32 bytes along K inside the 128B swizzle atom = +2 in the start field
             mma_bs_e<SF32>(tmem + buf * BN, adesc + (uint64_t)(k * 2), bdesc + (uint64_t)(k * 2), idesc,
-                           in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * (BN / 128));
+                           in_chunk > 0 ? 1u : 0u, sfa_col + atom * 4, sfb_col + atom * 4 * C::NRB);
             if (++in_chunk == chunk_len) in_chunk = 0;
           }
           ++kstep;
@@ -342,6 +354,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++s == n_stages) {  // tile done
           s = 0;
+          unit += unit_step;
           kstep = 0;
           in_chunk = 0;
           if (open) {
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       tc_fence_after();
       const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES + lane * 16;
       const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES + lane * 16;
-      const uint32_t col = lane_base + C::COL_SF + par * (C::SFA_COLS + C::SFB_COLS);
+      const uint32_t col = lane_base + C::COL_SF + par * C::SF_STRIDE;
       if (!(p.dbg & 16)) {
         uint32_t r[C::SFA_COLS];
 #pragma unroll
@@ -391,9 +404,9 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
 #pragma unroll
         for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at)
 #pragma unroll
-          for (int rb = 0; rb < BN / 128; ++rb) {
+          for (int rb = 0; rb < C::NRB; ++rb) {
             const uint4 w = ld_shared_u32x4(sfb_s + rb * C::SFA_BYTES + at * 512);
-            const int c = at * 4 * (BN / 128) + rb * 4;
+            const int c = at * 4 * C::NRB + rb * 4;
             r[c + 0] = w.x; r[c + 1] = w.y; r[c + 2] = w.z; r[c + 3] = w.w;
           }
         tmem_st<C::SFB_COLS>(col + C::SFA_COLS, r);
@@ -467,18 +480,29 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           store_row_bf16<COLS>(p, row, n0 + half * COLS, pk);
         } else
 #pragma unroll 1
-        for (int c = 0; c < COLS; c += 32) {
-          float v[32];
-          tmem_ld32(tmem_lane + buf * BN + c, v);
+        for (int c = 0; c < COLS; c += 16) {  // f32 out: 16 columns at a time (COLS may be 48)
+          float v[16];
+          tmem_ld16(tmem_lane + buf * BN + c, v);
           tmem_wait_ld();
-          if (c + 32 == COLS) {
+          if (c + 16 == COLS) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
           }
+          if (row < p.M && !(p.dbg & 4)) {
+            float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + n0 + half * COLS + c;
+            const int col = n0 + half * COLS + c;
+            if (col + 16 <= p.N && (p.ldc % 4) == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= scale_nv;
-          store_row32<OUT_BF16>(p, row, n0 + half * COLS + c, v);
+              for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4*>(out + i) =
+                    make_float4(v[i] * scale_nv, v[i + 1] * scale_nv, v[i + 2] * scale_nv, v[i + 3] * scale_nv);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (col + i < p.N) out[i] = v[i] * scale_nv;
+            }
+          }
         }
         if (++buf == NB) { buf = 0; tphase ^= 1; }
       } else if constexpr (MBS) {
@@ -674,6 +698,7 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.sfb = b.scales_mma;
   p.sfa_kg = a.sf_kpad / 4;
   p.sfb_kg = b.sf_kpad / 4;
+  p.sfb_rb = (int)((b.rows + 255) / 256 * 2);
   const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
   if constexpr (MBS) {
     const float* ones = ones_buffer();
