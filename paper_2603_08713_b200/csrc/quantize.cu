@@ -341,7 +341,7 @@ __device__ __forceinline__ void sq_unit(const Blk16<DT>& xb, bool active, const 
 
 template <int DT, int VAR, int G>
 __global__ void __launch_bounds__(SQ_THREADS) k_stream_quant(const void* __restrict__ x, int64_t x_ld, QDesc q,
-                                                             uint32_t nblk, uint32_t tpr, uint32_t ntiles,
+                                                             uint32_t nblk, FastDiv tpr, uint32_t ntiles,
                                                              uint32_t* __restrict__ status) {
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   uint32_t bad = 0, ovf_any = 0;
@@ -359,8 +359,8 @@ __global__ void __launch_bounds__(SQ_THREADS) k_stream_quant(const void* __restr
 #pragma unroll
     for (int u = 0; u < SQ_UNROLL; ++u) {
       const uint32_t t = t0 + u * gridDim.x;
-      rr[u] = t / tpr;
-      kk[u] = (t - rr[u] * tpr) * SQ_THREADS + tid;
+      rr[u] = fdiv(t, tpr);
+      kk[u] = (t - rr[u] * tpr.d) * SQ_THREADS + tid;
       if (t < ntiles && kk[u] < nblk) ld_blk<DT>(x, (int64_t)rr[u] * x_ld + kk[u] * 16, xb[u]);
       else zero_blk<DT>(xb[u]);
     }
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(SQ_THREADS) k_stream_quant(const void* __restr
 // floats) and the non-finite check, same tiling, one atomic per warp.
 template <int DT>
 __global__ void __launch_bounds__(SQ_THREADS) k_stream_absmax(const void* __restrict__ x, int64_t x_ld,
-                                                              uint32_t nblk, uint32_t tpr, uint32_t ntiles,
+                                                              uint32_t nblk, FastDiv tpr, uint32_t ntiles,
                                                               uint32_t* __restrict__ status) {
   const uint32_t tid = threadIdx.x;
   uint32_t bad = 0;
@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(SQ_THREADS) k_stream_absmax(const void* __rest
 #pragma unroll
     for (int u = 0; u < SQ_UNROLL; ++u) {
       const uint32_t t = t0 + u * gridDim.x;
-      const uint32_t r = t / tpr, kb = (t - r * tpr) * SQ_THREADS + tid;
+      const uint32_t r = fdiv(t, tpr), kb = (t - r * tpr.d) * SQ_THREADS + tid;
       if (t < ntiles && kb < nblk) ld_blk<DT>(x, (int64_t)r * x_ld + kb * 16, xb[u]);
       else zero_blk<DT>(xb[u]);
     }
@@ -451,7 +451,7 @@ __device__ __forceinline__ void nvfp4_unit(const Blk16<DT>& xb, bool active, con
 
 template <int DT>
 __global__ void __launch_bounds__(SQ_THREADS) k_stream_nvfp4(const void* __restrict__ x, int64_t x_ld, QDesc q,
-                                                             uint32_t nblk, uint32_t tpr, uint32_t ntiles,
+                                                             uint32_t nblk, FastDiv tpr, uint32_t ntiles,
                                                              const uint32_t* __restrict__ amax_bits) {
   const float amax = __uint_as_float(*amax_bits);
   const bool nz = amax > 0.0f;
@@ -466,8 +466,8 @@ __global__ void __launch_bounds__(SQ_THREADS) k_stream_nvfp4(const void* __restr
 #pragma unroll
     for (int u = 0; u < NV_UNROLL; ++u) {
       const uint32_t t = t0 + u * gridDim.x;
-      rr[u] = t / tpr;
-      kk[u] = (t - rr[u] * tpr) * SQ_THREADS + tid;
+      rr[u] = fdiv(t, tpr);
+      kk[u] = (t - rr[u] * tpr.d) * SQ_THREADS + tid;
       if (t < ntiles && kk[u] < nblk) ld_blk<DT>(x, (int64_t)rr[u] * x_ld + kk[u] * 16, xb[u]);
       else zero_blk<DT>(xb[u]);
     }
@@ -711,8 +711,9 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
   const bool bf = dtype == DT_BF16;
   // Row-tiled streaming grid (see k_stream_quant)
   const uint32_t nblk = (uint32_t)nbr16;
-  const uint32_t tpr = (uint32_t)((nbr16 + SQ_THREADS - 1) / SQ_THREADS);
-  const int64_t ntiles64 = rows * (int64_t)tpr;
+  const uint32_t tpr_n = (uint32_t)((nbr16 + SQ_THREADS - 1) / SQ_THREADS);
+  const FastDiv tpr = make_fastdiv(tpr_n);  // tiles per row (row index = tile / tpr)
+  const int64_t ntiles64 = rows * (int64_t)tpr_n;
   if (ntiles64 >= (int64_t)1 << 31) return set_error(ERR_UNSUPPORTED, "tensor too large");
   const uint32_t ntiles = (uint32_t)ntiles64;
   const int sq_grid = (int)std::min<int64_t>((ntiles + SQ_UNROLL - 1) / SQ_UNROLL, (int64_t)num_sms() * 8);
