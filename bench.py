@@ -122,10 +122,17 @@ def run_ours(args):
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
+    # one process per GPU; MXQ_DIST_BACKEND=gloo lets a single-GPU box run the
+    # multi-rank code path (ranks share the device) for testing
+    backend = os.environ.get("MXQ_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     V = M.Variant
     bf16 = torch.bfloat16
 
@@ -181,7 +188,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     graphs = {}
@@ -361,7 +371,7 @@ def run_ours(args):
                "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)) * world,
                "ms_per_step": ms_e2e, "wall_ms_per_step": wall}
     if world > 1:
-        dist.barrier(device_ids=[local])
+        barrier()
 
     if rank != 0:
         if world > 1:

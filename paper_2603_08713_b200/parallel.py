@@ -87,6 +87,8 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     """Timing reduction: every multi-GPU time is the max over ranks."""
     if not (dist.is_available() and dist.is_initialized()):
         return value
+    if dist.get_backend(group) == "gloo":
+        device = None  # gloo reduces host tensors
     t = torch.tensor([value], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
