@@ -11,27 +11,28 @@
 //
 // That FP32 work bounds the kernel: 128 FP32 lanes/clk/SM against 16384 FP4
 // MACs/clk/SM means 2*BM*BN/128 cycles of FP32 per chunk versus BM*BN*128/16384
-// of MMA -- the tensor pipe can be at most 50 % busy.  The
-// structure is chosen so that nothing else binds first:
+// of MMA -- the tensor pipe can be at most 50 % busy:
 //   * 128 x 192 tiles, N=192 MMAs (96 cycles each, long enough to hide the
 //     issuing thread's ~70-cycle per-MMA cost that made N=128 MMAs issue-bound),
-//     two 192-column TMEM partial buffers and two 48-column scale-factor
-//     buffers (384 + 2*64 columns <= 512);
+//     two 192-column TMEM partial buffers and two 64-column-aligned
+//     scale-factor buffers (384 + 2*64 columns <= 512);
+//   * scale factors reach TMEM by tcgen05.cp from the MMA warp, in order with
+//     the MMAs: the tensor pipe has the slack, the epilogue does not;
 //   * 16 epilogue warps (4 per TMEM lane quadrant, 48 columns each) hold the
-//     48 f32 accumulators and load a chunk's whole partial (48 registers) before
-//     releasing its TMEM buffer, so the next-but-one chunk's MMAs start early;
-//     setmaxnreg gives them 112 registers and the 4 control warps 32 (the pool is
-//     the 96 x 640 registers allocated at launch);
-//   * the epilogue warps also move each stage's scale factors smem -> TMEM
-//     (tcgen05.st, 3 atoms per warp per stage): tcgen05.cp costs ~64 tensor-pipe
-//     cycles per 512-byte atom (tools/microbench_cp.cu) and dedicated writer
-//     warps would cost the registers the accumulators need;
-//   * clusters of 2 CTAs share the B tile by TMA multicast.
+//     48 f32 accumulators and load a chunk's whole partial before releasing its
+//     TMEM buffer; setmaxnreg gives them 112 registers and the 4 control warps
+//     32 (the pool is the 96 x 640 registers allocated at launch);
+//   * clusters of 2 CTAs share the B tile by TMA multicast;
+//   * few-tile shapes (small M: decode / expert GEMMs) split K over CTAs at
+//     stage boundaries, write f32 partials and sum them in a fixed order
+//     (k_splitk_reduce), so every SM streams weights.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
@@ -48,14 +49,9 @@ constexpr int NSFB = 2, NSIG = 8;
 constexpr int ATOM = 512;                   // SF atom: 128 rows x 4 blocks of 16
 constexpr int STAGE_A = BM * KSTAGE / 2;    // 16 KB of A codes per stage
 constexpr int SFA_BYTES = 4 * ATOM;         // 4 k-steps
-// Scale factors reach TMEM by tcgen05.cp issued from the MMA warp (in order
-// with the MMAs, ~64 tensor-pipe cycles per atom, tools/microbench_cp.cu) --
-// the tensor pipe has the slack, the epilogue warps do not -- instead of
-// tcgen05.st from the epilogue warps (false).
-constexpr bool SF_CP = true;
-
-// Tile shape (BN output columns, NB TMEM partial buffers).  The product path
-// is BN=192, NB=2 (DESIGN.md section 3 lists the measured alternatives).
+// Tile shape (BN output columns, NB TMEM partial buffers, EPIW epilogue
+// warps).  The product path is <192, 2, 16> (DESIGN.md section 3.4 lists the
+// measured alternatives).
 template <int BN_, int NB_, int EPIW_>
 struct MbsCfg {
   static constexpr int BN = BN_, NB = NB_;
@@ -74,7 +70,7 @@ struct MbsCfg {
   static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
   static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
   static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + NSFB;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
   // TMEM: partial buffers [0, NB*BN), SF buffers 64-aligned after them
   // (misaligned SF addresses slow the MMA, tools/microbench_mma3.cu).  Within
@@ -84,10 +80,9 @@ struct MbsCfg {
   // EPIW*32*EPI + 4*32*CTRL must fit the registers allocated at launch
   // (ptxas' per-thread count x THREADS: 96 x 640 for 16 epilogue warps,
   // 168 x 384 for 8) -- setmaxnreg.inc blocks forever otherwise
-  static constexpr bool SETMAXNREG = COLS > 32 || NB >= 3;  // NB >= 3 keeps two partials in registers
+  static constexpr bool SETMAXNREG = COLS > 32;
   static constexpr int EPI_REGS = EPIW == 16 ? 112 : 208, CTRL_REGS = EPIW == 16 ? 32 : 48;
   static_assert(EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= (EPIW == 16 ? 96 * 640 : 168 * 384), "register pool");
-  static_assert(SF_CP || EPIW == 16, "epilogue SF writing assigns one k-step per column group");
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(OFF_B % 1024 == 0 && STAGE_B % 1024 == 0 && (BN / 2) * 128 % 1024 == 0, "128B-swizzle alignment");
   static_assert(COL_SF0 + NSFB * SF_STRIDE <= 512, "TMEM budget");
@@ -105,8 +100,11 @@ struct Params {
   void* c;
   int64_t ldc;
   int M, N, K;
-  int mac_steps;       // macro size / 64
+  int mac_steps;       // macro size / 64 (1, 2 or 4: chunks never straddle a 256-K stage)
   int n_chunks;        // macros per row
+  int ksplit;          // K splits (stage-aligned); > 1: f32 partials to ws[split][M][ws_ld]
+  float* ws;
+  int64_t ws_ld;
   uint32_t idesc;
   long long* trace;    // clock64 trace of CTA 0 (MXQ_GEMM_TRACE builds only)
 };
@@ -127,16 +125,6 @@ __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.
 template <int R>
 __device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R)); }
 
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint4 w) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(w.x), "r"(w.y), "r"(w.z),
-               "r"(w.w)
-               : "memory");
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint4 a, uint4 b) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a.x),
-               "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
-               : "memory");
-}
 __device__ __forceinline__ void mbar_init_a(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -187,22 +175,37 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
   const uint32_t a_full = a_smem + OFF_BAR, a_empty = a_full + 8 * STAGES;
   const uint32_t a_tfull = a_empty + 8 * STAGES, a_tempty = a_tfull + 8 * NB;
   const uint32_t a_sfull = a_tempty + 8 * NB, a_sempty = a_sfull + 8 * NSIG;
-  const uint32_t a_sfready = a_sempty + 8 * NSIG;
-  const uint32_t a_tmem_slot = a_sfready + 8 * NSFB;
+  const uint32_t a_tmem_slot = a_sempty + 8 * NSIG;
 
   // warp index through a shuffle so ptxas knows it is warp-uniform
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
   const int groups_m = (tiles_m + CL - 1) / CL;
-  const int num_units = groups_m * tiles_n;
+  const int ksplit = p.ksplit;
+  const int num_units = groups_m * tiles_n * ksplit;
   const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
   uint32_t crank = 0;
   if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
   const int n_ksteps = (p.K + KSTEP - 1) / KSTEP;
   const int n_stages = (p.K + KSTAGE - 1) / KSTAGE;
   const int n_chunks = p.n_chunks, mac_steps = p.mac_steps;
-  const int my_units = unit0 < num_units ? (num_units - 1 - unit0) / unit_step + 1 : 0;
-  const int total_chunks = my_units * n_chunks;
+  const int cps = 4 / mac_steps;                             // chunks per 256-K stage
+  const int spl = (n_stages + ksplit - 1) / ksplit;         // stages per K split
+  // A work unit: one (128-row group, BN-column tile, K split) of the output;
+  // the CTAs of a cluster take consecutive 128-row blocks of it.
+  struct Unit { int mb, nb, split, s_lo, s_hi, c_lo, c_hi; };
+  auto unit_of = [&](int u) {
+    Unit r;
+    r.split = u % ksplit;
+    const int rest = u / ksplit;
+    r.mb = (rest % groups_m) * CL + (int)crank;
+    r.nb = rest / groups_m;
+    r.s_lo = r.split * spl;
+    r.s_hi = min(r.s_lo + spl, n_stages);
+    r.c_lo = r.s_lo * cps;
+    r.c_hi = min(r.s_hi * cps, n_chunks);
+    return r;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -217,7 +220,6 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
       mbar_init_a(a_sfull + 8 * b, 1);
       mbar_init_a(a_sempty + 8 * b, EPIW);
     }
-    for (int b = 0; b < NSFB; ++b) mbar_init_a(a_sfready + 8 * b, EPIW);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -238,22 +240,21 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
       // ===================== TMA producer =====================
       uint32_t st = 0, ph = 0, slot = 0, sph = 0;
       for (int unit = unit0; unit < num_units; unit += unit_step) {
-        const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
-        const int m0 = mb * BM, n0 = nb * BN;
+        const Unit U = unit_of(unit);
+        const int m0 = U.mb * BM, n0 = U.nb * BN;
         const int rb0 = n0 / 128;
         const int nrb = (rb0 + NRB <= p.sfb_rb) ? NRB : p.sfb_rb - rb0;
         const uint32_t tx = STAGE_A + STAGE_B + SFA_BYTES + nrb * 4 * ATOM;
-        const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * ATOM;
+        const uint8_t* sa = p.sfa + (int64_t)U.mb * p.sfa_kg * ATOM;
         const uint8_t* sb = p.sfb + (int64_t)rb0 * p.sfb_kg * ATOM;
         const float* ga = p.sga + (p.sga_ld ? m0 : 0);
         const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
         int sb_bytes = BN * 4;
         if (p.sgb_ld && p.sgb_ld - n0 < BN) sb_bytes = (int)(p.sgb_ld - n0) * 4;
-        int chunk = 0;
-        for (int s = 0; s < n_stages; ++s) {
+        int chunk = U.c_lo;
+        for (int s = U.s_lo; s < U.s_hi; ++s) {
           const uint32_t fb = a_full + st * 8;
           mbar_wait_a(a_empty + st * 8, ph ^ 1);
-          trace_at(p, (uint32_t)((unit - unit0) / unit_step * n_chunks + chunk), 12);
           expect_tx_e(fb, tx);
           tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, &tmA, fb, s * (KSTAGE / 2), m0);
           if constexpr (CL == 1) {
@@ -268,14 +269,13 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
                         sb + ((int64_t)r * p.sfb_kg + (int64_t)s * 4) * ATOM, 4 * ATOM, fb);
           if (++st == STAGES) { st = 0; ph ^= 1; }
           // sigma slices of the chunks that start in this stage
-          while (chunk < n_chunks && chunk * mac_steps < 4 * (s + 1)) {
+          while (chunk < U.c_hi && chunk * mac_steps < 4 * (s + 1)) {
             const uint32_t sfb = a_sfull + slot * 8;
             mbar_wait_a(a_sempty + slot * 8, sph ^ 1);
             expect_tx_e(sfb, BM * 4 + sb_bytes);
             const uint32_t dst = a_smem + OFF_SIG + slot * SIG_SLOT;
             bulk_load_e(dst, ga + (int64_t)chunk * p.sga_ld, BM * 4, sfb);
             bulk_load_e(dst + BM * 4, gb + (int64_t)chunk * p.sgb_ld, sb_bytes, sfb);
-            trace_at(p, (uint32_t)((unit - unit0) / unit_step * n_chunks + chunk), 11);
             if (++slot == NSIG) { slot = 0; sph ^= 1; }
             ++chunk;
           }
@@ -283,17 +283,17 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
       }
     } else if (warp == W_MMA) {
       // ===================== MMA issuer =====================
-      uint32_t g = 0;  // global stage counter (smem ring and SF buffers)
+      uint32_t g = 0;             // stages consumed (SF buffer parity)
       uint32_t buf = 0, tph = 0;  // TMEM partial-buffer ring
-      uint32_t st = 0;
-      uint32_t q = 0;
+      uint32_t st = 0;            // smem ring position
+      uint32_t q = 0;             // chunks issued (trace only)
       for (int unit = unit0; unit < num_units; unit += unit_step) {
-        const int nb = unit / groups_m;
-        const uint32_t sfb_shift = ((nb * BN) % 128) ? 2u : 0u;  // odd 192-tiles start 64 rows into the atom
-        int ks = 0;
+        const Unit U = unit_of(unit);
+        const uint32_t sfb_shift = ((U.nb * BN) % 128) ? 2u : 0u;  // odd 192-tiles start 64 rows into the atom
+        int ks = U.s_lo * 4;
         uint64_t adesc = 0, bdesc = 0;
         uint32_t sfa_col = 0;
-        for (int c = 0; c < n_chunks; ++c, ++q) {
+        for (int c = U.c_lo; c < U.c_hi; ++c, ++q) {
           const uint32_t dcol = tmem + buf * BN;
           trace_at(p, q, 0);
           mbar_wait_a(a_tempty + buf * 8, tph ^ 1u);
@@ -305,24 +305,18 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
           for (; ks < kend; ++ks) {
             const uint32_t j = (uint32_t)ks & 3u;
             if (j == 0) {
+              // this stage's SF atoms -> SF buffer g % 2 (the buffer's previous
+              // readers, stage g-2's MMAs, precede these copies in the pipe)
               sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
-              if constexpr (SF_CP) {
-                mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
-                trace_at(p, q, 10);
-                tc_fence_after();
-                // this stage's SF atoms -> SF buffer g % 2 (the buffer's previous
-                // readers, stage g-2's MMAs, precede these copies in the pipe)
+              mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
+              trace_at(p, q, 10);
+              tc_fence_after();
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj) {
-                  sf_cp_e(sfa_col + 4 * jj, a_smem + OFF_SFA + st * SFA_BYTES + jj * ATOM);
+              for (int jj = 0; jj < 4; ++jj) {
+                sf_cp_e(sfa_col + 4 * jj, a_smem + OFF_SFA + st * SFA_BYTES + jj * ATOM);
 #pragma unroll
-                  for (int r = 0; r < NRB; ++r)
-                    sf_cp_e(sfa_col + 16 + 4 * NRB * jj + 4 * r, a_smem + OFF_SFB + st * SFB_BYTES + r * 4 * ATOM + jj * ATOM);
-                }
-              } else {
-                mbar_wait_a(a_sfready + (g & (NSFB - 1)) * 8, (g / NSFB) & 1u);
-                trace_at(p, q, 10);
-                tc_fence_after();
+                for (int r = 0; r < NRB; ++r)
+                  sf_cp_e(sfa_col + 16 + 4 * NRB * jj + 4 * r, a_smem + OFF_SFB + st * SFB_BYTES + r * 4 * ATOM + jj * ATOM);
               }
               adesc = operand_desc(a_smem + OFF_A + st * STAGE_A);
               bdesc = operand_desc(a_smem + OFF_B + st * STAGE_B);
@@ -343,147 +337,74 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
       }
     }
   } else {
-    // ===================== epilogue (warps 0..15) =====================
+    // ===================== epilogue (warps 0..EPIW-1) =====================
     if constexpr (C::SETMAXNREG) setmaxnreg_inc<C::EPI_REGS>();
     const int quad = warp & 3, grp = warp >> 2;  // TMEM lane quadrant, column group
-    const uint32_t t_lane = tmem + ((uint32_t)(quad * 32) << 16);
-    const uint32_t t_ld = t_lane + grp * COLS;
+    const uint32_t t_ld = tmem + ((uint32_t)(quad * 32) << 16) + grp * COLS;
     const int row_in_tile = quad * 32 + lane;
     const uint32_t sig_a = a_smem + OFF_SIG + row_in_tile * 4;
     const uint32_t sig_b = a_smem + OFF_SIG + (BM + grp * COLS) * 4;
-    // Scale factors of global stage `sf_next`: this warp moves k-step `grp`
-    // (one SFA atom, NRB SFB atoms) into its lane quadrant of SF buffer
-    // sf_next % 2, then arrives on sf_ready (16 arrivals per stage).
-    uint32_t sf_next = 0;
-    auto write_sf_upto = [&](uint32_t upto) {
-      while (sf_next <= upto) {
-        const uint32_t st = sf_next % STAGES;
-        mbar_wait_a(a_full + st * 8, (sf_next / STAGES) & 1u);
-        const uint32_t sf_lane = lane * 16 + grp * ATOM;
-        const uint4 wa = ld_shared_u32x4(a_smem + OFF_SFA + st * SFA_BYTES + sf_lane);
-        const uint4 wb0 = ld_shared_u32x4(a_smem + OFF_SFB + st * SFB_BYTES + sf_lane);
-        const uint32_t col = t_lane + COL_SF0 + (sf_next & (NSFB - 1)) * SF_STRIDE;
-        tmem_st4(col + 4 * grp, wa);
-        if constexpr (NRB == 2) {
-          const uint4 wb1 = ld_shared_u32x4(a_smem + OFF_SFB + st * SFB_BYTES + 4 * ATOM + sf_lane);
-          tmem_st8(col + 16 + 8 * grp, wb0, wb1);
-        } else {
-          tmem_st4(col + 16 + 4 * grp, wb0);
-        }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        arrive_e(a_sfready + (sf_next & (NSFB - 1)) * 8);
-        ++sf_next;
-      }
-    };
-    // Chunk q + NB (tile ordinal nx_t, chunk nx_c): the chunk whose MMAs the
-    // release of chunk q's partial buffer lets start.
-    int nx_t = 0, nx_c = 0;
-    auto nx_stage = [&]() -> uint32_t {
-      int last = (nx_c + 1) * mac_steps;
-      if (last > n_ksteps) last = n_ksteps;
-      return (uint32_t)(nx_t * n_stages + ((last - 1) >> 2));
-    };
-    auto nx_advance = [&]() {
-      if (++nx_c == n_chunks) { nx_c = 0; ++nx_t; }
-    };
-    if (!SF_CP && total_chunks > 0) {
-      for (int i = 0; i < NB && i < total_chunks; ++i) {
-        write_sf_upto(nx_stage());
-        nx_advance();
-      }
-    }
-
-    // Load side (TMEM partial buffers) and compute side (sigma ring) counters.
-    uint32_t ql = 0, lbuf = 0, ltph = 0;   // next chunk to load
-    uint32_t qc = 0, slot = 0, sph = 0;    // next chunk to compute
-    auto start_load = [&](float* v) {
-      if (warp == 0) trace_at(p, ql, 3);
-      mbar_wait_a(a_tfull + lbuf * 8, ltph);
-      if (warp == 0) trace_at(p, ql, 4);
-      if (warp == EPIW - 1) trace_at(p, ql, 8);
-      tc_fence_after();
-      // chunk ql is complete, so every MMA of the stages before it is too: the
-      // SF buffer of chunk ql+NB's stage can be overwritten now (before the
-      // release below lets chunk ql+NB's MMAs start; they wait for these).
-      if (!SF_CP && (int)ql + NB < total_chunks) {
-        write_sf_upto(nx_stage());
-        nx_advance();
-      }
-#pragma unroll
-      for (int h = 0; h < COLS / 16; ++h) tmem_ld16_nw(t_ld + lbuf * BN + h * 16, v + h * 16);
-    };
-    auto finish_load = [&](float* v) {
-      tmem_wait_ld();
-      reg_fence<COLS>(v);
-      tc_fence_before();
-      __syncwarp();
-      arrive_e(a_tempty + lbuf * 8);
-      if (warp == 0) trace_at(p, ql, 5);
-      ++ql;
-      if (++lbuf == NB) { lbuf = 0; ltph ^= 1; }
-    };
-    // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
-    auto compute = [&](float* acc, const float* v) {
-      mbar_wait_a(a_sfull + slot * 8, sph);
-      if (warp == 0) trace_at(p, qc, 6);
-      const uint32_t so = slot * SIG_SLOT;
-      const float sa = ld_shared_f32(sig_a + so);
-#pragma unroll
-      for (int i = 0; i < COLS; i += 4) {
-        const float4 sb = ld_shared_f32x4(sig_b + so + i * 4);
-        float w0, w1, w2, w3;
-        mul2(w0, w1, sa, sb.x, sb.y);
-        mul2(w2, w3, sa, sb.z, sb.w);
-        fma2(acc[i], acc[i + 1], w0, w1, v[i], v[i + 1]);
-        fma2(acc[i + 2], acc[i + 3], w2, w3, v[i + 2], v[i + 3]);
-      }
-      __syncwarp();
-      arrive_e(a_sempty + slot * 8);
-      if (warp == 0) trace_at(p, qc, 7);
-      if (warp == EPIW - 1) trace_at(p, qc, 9);
-      ++qc;
-      if (++slot == NSIG) { slot = 0; sph ^= 1; }
-    };
+    uint32_t q = 0, lbuf = 0, ltph = 0, slot = 0, sph = 0;
 
     for (int unit = unit0; unit < num_units; unit += unit_step) {
-      const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
-      const int row = mb * BM + row_in_tile;
-      const int col0 = nb * BN + grp * COLS;
+      const Unit U = unit_of(unit);
+      const int row = U.mb * BM + row_in_tile;
+      const int col0 = U.nb * BN + grp * COLS;
       float acc[COLS];
 #pragma unroll
       for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
-      if constexpr (NB >= 3) {
-        // two register sets: the TMEM loads of chunk c+1 are in flight while
-        // chunk c is folded (the MMA runs NB-1 chunks ahead, so they are ready)
-        float pa[COLS], pb[COLS];
-        start_load(pa);
-        finish_load(pa);
-        int c = 0;
 #pragma unroll 1
-        while (true) {
-          if (c + 1 < n_chunks) start_load(pb);
-          compute(acc, pa);
-          if (++c == n_chunks) break;
-          finish_load(pb);
-          if (c + 1 < n_chunks) start_load(pa);
-          compute(acc, pb);
-          if (++c == n_chunks) break;
-          finish_load(pa);
+      for (int c = U.c_lo; c < U.c_hi; ++c, ++q) {
+        // the chunk's partial: load all of it, then release the TMEM buffer
+        if (warp == 0) trace_at(p, q, 3);
+        mbar_wait_a(a_tfull + lbuf * 8, ltph);
+        if (warp == 0) trace_at(p, q, 4);
+        if (warp == EPIW - 1) trace_at(p, q, 8);
+        tc_fence_after();
+        float v[COLS];
+#pragma unroll
+        for (int h = 0; h < COLS / 16; ++h) tmem_ld16_nw(t_ld + lbuf * BN + h * 16, v + h * 16);
+        tmem_wait_ld();
+        reg_fence<COLS>(v);
+        tc_fence_before();
+        __syncwarp();
+        arrive_e(a_tempty + lbuf * 8);
+        if (warp == 0) trace_at(p, q, 5);
+        if (++lbuf == NB) { lbuf = 0; ltph ^= 1; }
+        // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
+        mbar_wait_a(a_sfull + slot * 8, sph);
+        if (warp == 0) trace_at(p, q, 6);
+        const uint32_t so = slot * SIG_SLOT;
+        const float sa = ld_shared_f32(sig_a + so);
+#pragma unroll
+        for (int i = 0; i < COLS; i += 4) {
+          const float4 sb = ld_shared_f32x4(sig_b + so + i * 4);
+          float w0, w1, w2, w3;
+          mul2(w0, w1, sa, sb.x, sb.y);
+          mul2(w2, w3, sa, sb.z, sb.w);
+          fma2(acc[i], acc[i + 1], w0, w1, v[i], v[i + 1]);
+          fma2(acc[i + 2], acc[i + 3], w2, w3, v[i + 2], v[i + 3]);
         }
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < n_chunks; ++c) {
-          float v[COLS];
-          start_load(v);
-          finish_load(v);
-          compute(acc, v);
-        }
+        __syncwarp();
+        arrive_e(a_sempty + slot * 8);
+        if (warp == 0) trace_at(p, q, 7);
+        if (warp == EPIW - 1) trace_at(p, q, 9);
+        if (++slot == NSIG) { slot = 0; sph ^= 1; }
       }
-      // store the tile row (masked to M x N)
+      // store the tile row (masked to M x N): the output, or this split's f32 partial
       if (row < p.M) {
-        if constexpr (OUT_BF16) {
+        if (ksplit > 1) {
+          float* out = p.ws + ((int64_t)U.split * p.M + row) * p.ws_ld + col0;
+          if (col0 + COLS <= p.N) {
+#pragma unroll
+            for (int i = 0; i < COLS; i += 4)
+              *reinterpret_cast<float4*>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < COLS; ++i)
+              if (col0 + i < p.N) out[i] = acc[i];
+          }
+        } else if constexpr (OUT_BF16) {
           __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
           if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
 #pragma unroll
@@ -525,8 +446,43 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
   }
 }
 
+// Split-K partials: C = sum over splits (ascending) of ws[split], as bf16 or f32.
+template <bool OUT_BF16>
+__global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__ ws, int ksplit, int M, int N,
+                                                       int64_t ws_ld, void* __restrict__ c, int64_t ldc) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / N, col = i - r * N;
+    float acc = ws[r * ws_ld + col];
+    for (int sp = 1; sp < ksplit; ++sp) acc += ws[((int64_t)sp * M + r) * ws_ld + col];
+    if constexpr (OUT_BF16) reinterpret_cast<__nv_bfloat16*>(c)[r * ldc + col] = __float2bfloat16_rn(acc);
+    else reinterpret_cast<float*>(c)[r * ldc + col] = acc;
+  }
+}
+
+// Per-device f32 workspace for split-K partials, grown outside graph capture.
+static float* splitk_workspace(size_t bytes, cudaStream_t st) {
+  static float* ptr[64] = {nullptr};
+  static size_t cap[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (cap[dev] >= bytes) return ptr[dev];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  if (ptr[dev]) {
+    cudaStreamSynchronize(st);
+    cudaFree(ptr[dev]);
+  }
+  ptr[dev] = nullptr;
+  cap[dev] = 0;
+  if (cudaMalloc(&ptr[dev], bytes) != cudaSuccess) return nullptr;
+  cap[dev] = bytes;
+  return ptr[dev];
+}
+
 template <int BN, int NB, int EPIW, bool OUT_BF16, int CL>
-static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStream_t st) {
+static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int ksplit, float* ws, cudaStream_t st) {
   using C = MbsCfg<BN, NB, EPIW>;
   constexpr int SMEM = C::SMEM;
   auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL>;
@@ -562,10 +518,13 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStre
   const int macro = ma ? a.macro_size : b.macro_size;
   p.mac_steps = macro / KSTEP;
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
-  // E2M1 x E2M1, UE8M0 scales, N = 192, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
+  p.ksplit = ksplit;
+  p.ws = ws;
+  p.ws_ld = p.N;
   p.trace = g_trace;
+  // E2M1 x E2M1, UE8M0 scales, N = BN, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
   p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
-  const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
+  const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN) * ksplit;
   int clusters = num_sms() / CL;
   if (units < clusters) clusters = units;
   cudaLaunchConfig_t cfg = {};
@@ -582,13 +541,18 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStre
   cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, p);
   if (e != cudaSuccess) return set_cuda_error(e);
+  if (ksplit > 1) {
+    const int64_t total = (int64_t)p.M * p.N;
+    int g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+    k_splitk_reduce<OUT_BF16><<<g, 256, 0, st>>>(ws, ksplit, p.M, p.N, p.ws_ld, c, ldc);
+  }
   return check_launch();
 }
 
 }  // namespace mbs
 
-// MBS pair on the tcgen05 path: macro sizes 64, 128, 256 (two SF buffers
-// cover at most one stage of look-ahead; other sizes take the exact kernel).
+// MBS pair on the tcgen05 path: macro sizes 64, 128, 256 (chunks never
+// straddle a 256-K stage; other sizes take the first-generation kernel).
 bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
   const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
   if (!ma && !mb) return false;
@@ -599,15 +563,34 @@ bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
 }
 
 int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
-  static int shape = -1;  // development A/B (MXQ_GEMM_MBS_SHAPE): 1 = 16 warps x 48 cols, 2 = 8 warps x 96, 3 = 128x128 NB=3
-  if (shape < 0) {
-    const char* d = getenv("MXQ_GEMM_MBS_SHAPE");
-    shape = d ? atoi(d) : 1;
-  }
+  constexpr int BN = 192;
   const bool bf = c_dtype == MXQ_BF16;
-  if (shape == 2) return bf ? mbs::launch<192, 2, 8, true, 2>(a, b, c, ldc, st) : mbs::launch<192, 2, 8, false, 2>(a, b, c, ldc, st);
-  if (shape == 3) return bf ? mbs::launch<128, 3, 16, true, 2>(a, b, c, ldc, st) : mbs::launch<128, 3, 16, false, 2>(a, b, c, ldc, st);
-  return bf ? mbs::launch<192, 2, 16, true, 2>(a, b, c, ldc, st) : mbs::launch<192, 2, 16, false, 2>(a, b, c, ldc, st);
+  const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM), tiles_n = (int)((b.rows + BN - 1) / BN);
+  const int n_stages = (int)((a.cols + mbs::KSTAGE - 1) / mbs::KSTAGE);
+  // one 128-row block: no pairing across M, so no cluster (its second CTA would idle)
+  const int CL = tiles_m >= 2 ? 2 : 1;
+  const int base = ((tiles_m + CL - 1) / CL) * tiles_n;  // clusters' worth of work without splitting K
+  const int slots = num_sms() / CL;
+  // Few tiles and few rows (decode-like M <= 64): split K at stage boundaries
+  // so every SM streams weights.  (At M = 128 the extra f32 partial traffic
+  // and the reduce cost more than the parallelism wins: 18 vs 21 us on the
+  // GPT-OSS gate_up shape, profiles/configs_r01.json.)
+  int ksplit = 1;
+  if (a.rows <= 64 && 2 * base <= slots && n_stages >= 4) {
+    ksplit = std::min(slots / base, n_stages / 2);
+    const int spl = (n_stages + ksplit - 1) / ksplit;
+    ksplit = (n_stages + spl - 1) / spl;  // no empty split
+  }
+  float* ws = nullptr;
+  if (ksplit > 1) {
+    ws = mbs::splitk_workspace((size_t)ksplit * a.rows * b.rows * sizeof(float), st);
+    if (!ws) ksplit = 1;  // (first use inside a graph capture: run unsplit)
+  }
+  if (CL == 1)
+    return bf ? mbs::launch<BN, 2, 16, true, 1>(a, b, c, ldc, ksplit, ws, st)
+              : mbs::launch<BN, 2, 16, false, 1>(a, b, c, ldc, ksplit, ws, st);
+  return bf ? mbs::launch<BN, 2, 16, true, 2>(a, b, c, ldc, ksplit, ws, st)
+            : mbs::launch<BN, 2, 16, false, 2>(a, b, c, ldc, ksplit, ws, st);
 }
 
 }  // namespace mxq

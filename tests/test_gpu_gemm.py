@@ -124,3 +124,22 @@ def test_tc_gemm_mbs_persistent_tiles(va, vb):
     _check(c, want, bound, (va, vb, "persistent"))
     cb = M.matmul_quantized(aq, bq, out_dtype=torch.bfloat16).float().cpu().numpy()
     assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
+
+
+@pytest.mark.parametrize("m", [1, 8, 128])
+def test_tc_gemm_mbs_small_m_split_k(m):
+    """GPT-OSS expert shapes (config 5): one 128-row block, K = 2880 split across
+    CTAs at stage boundaries (f32 partials summed in a fixed order); the last
+    macro is 64 wide.  Same tolerance as every tcgen05 product, deterministic."""
+    rng = np.random.Generator(np.random.PCG64(31 + m))
+    for n in (5760, 2880):
+        a = rng.standard_t(4, (m, 2880)).astype(np.float32)
+        b = (rng.standard_normal((n, 2880)) * 0.02).astype(np.float32)
+        aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S))
+        bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant.MBS_D))
+        c = M.matmul_quantized(aq, bq).cpu().numpy()
+        want, bound = _ref(a, b, "mbs_s", "mbs_d")
+        _check(c, want, bound, ("small-m", m, n))
+        assert np.array_equal(c, M.matmul_quantized(aq, bq).cpu().numpy())
+        cb = M.matmul_quantized(aq, bq, out_dtype=torch.bfloat16).float().cpu().numpy()
+        assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
