@@ -60,7 +60,7 @@ struct MbsCfg {
   static constexpr int THREADS = (EPIW + 4) * 32;
   static constexpr int COLS = BN / (EPIW / 4);          // output columns per epilogue thread
   static constexpr int NRB = BN / 128 + (BN % 128 ? 1 : 0);  // 128-row SF atoms a tile can touch
-  static constexpr int STAGES = BN > 128 ? 4 : 5;
+  static constexpr int STAGES = BN > 128 ? 4 : (BN > 64 ? 5 : 7);  // narrow (decode) tiles: deeper weight prefetch
   static constexpr int STAGE_B = BN * KSTAGE / 2;
   static constexpr int SFB_BYTES = NRB * 4 * ATOM;     // NRB row blocks x 4 k-steps
   static constexpr int SIG_SLOT = (BM + BN) * 4;       // sigmaA[128] + sigmaB[BN], f32
@@ -80,7 +80,7 @@ struct MbsCfg {
   // EPIW*32*EPI + 4*32*CTRL must fit the registers allocated at launch
   // (ptxas' per-thread count x THREADS: 96 x 640 for 16 epilogue warps,
   // 168 x 384 for 8) -- setmaxnreg.inc blocks forever otherwise
-  static constexpr bool SETMAXNREG = COLS > 32;
+  static constexpr bool SETMAXNREG = COLS > 32 && EPIW > 4;
   static constexpr int EPI_REGS = EPIW == 16 ? 112 : 208, CTRL_REGS = EPIW == 16 ? 32 : 48;
   static_assert(EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= (EPIW == 16 ? 96 * 640 : 168 * 384), "register pool");
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -159,7 +159,10 @@ __device__ __forceinline__ void reg_fence(float* v) {
                  "+f"(v[i + 6]), "+f"(v[i + 7]));
 }
 
-template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL>
+// TRANS: swap-AB for decode-sized M -- the kernel's A operand is the weight
+// matrix (128 weight rows per tile) and its B operand the few activation rows
+// (BN >= M), so the output tile is stored transposed into C[token][n].
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS>
 __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
     k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
   using C = MbsCfg<BN_, NB_, EPIW_>;
@@ -392,7 +395,26 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
         if (++slot == NSIG) { slot = 0; sph ^= 1; }
       }
       // store the tile row (masked to M x N): the output, or this split's f32 partial
-      if (row < p.M) {
+      if (TRANS && row < p.M) {
+        // kernel row = weight row n, kernel column = token: C[token][n] (and the
+        // split partials in the same output orientation)
+        if (ksplit > 1) {
+          float* out = p.ws + ((int64_t)U.split * p.N + col0) * p.ws_ld + row;
+#pragma unroll
+          for (int i = 0; i < COLS; ++i)
+            if (col0 + i < p.N) out[(int64_t)i * p.ws_ld] = acc[i];
+        } else if constexpr (OUT_BF16) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)col0 * p.ldc + row;
+#pragma unroll
+          for (int i = 0; i < COLS; ++i)
+            if (col0 + i < p.N) out[(int64_t)i * p.ldc] = __float2bfloat16_rn(acc[i]);
+        } else {
+          float* out = reinterpret_cast<float*>(p.c) + (int64_t)col0 * p.ldc + row;
+#pragma unroll
+          for (int i = 0; i < COLS; ++i)
+            if (col0 + i < p.N) out[(int64_t)i * p.ldc] = acc[i];
+        }
+      } else if (row < p.M) {
         if (ksplit > 1) {
           float* out = p.ws + ((int64_t)U.split * p.M + row) * p.ws_ld + col0;
           if (col0 + COLS <= p.N) {
@@ -481,11 +503,11 @@ static float* splitk_workspace(size_t bytes, cudaStream_t st) {
   return ptr[dev];
 }
 
-template <int BN, int NB, int EPIW, bool OUT_BF16, int CL>
+template <int BN, int NB, int EPIW, bool OUT_BF16, int CL, bool TRANS>
 static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int ksplit, float* ws, cudaStream_t st) {
   using C = MbsCfg<BN, NB, EPIW>;
   constexpr int SMEM = C::SMEM;
-  auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL>;
+  auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL, TRANS>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -520,7 +542,7 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.ksplit = ksplit;
   p.ws = ws;
-  p.ws_ld = p.N;
+  p.ws_ld = TRANS ? p.M : p.N;
   p.trace = g_trace;
   // E2M1 x E2M1, UE8M0 scales, N = BN, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
   p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
@@ -544,7 +566,8 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   if (ksplit > 1) {
     const int64_t total = (int64_t)p.M * p.N;
     int g = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-    k_splitk_reduce<OUT_BF16><<<g, 256, 0, st>>>(ws, ksplit, p.M, p.N, p.ws_ld, c, ldc);
+    if (TRANS) k_splitk_reduce<OUT_BF16><<<g, 256, 0, st>>>(ws, ksplit, p.N, p.M, p.ws_ld, c, ldc);
+    else k_splitk_reduce<OUT_BF16><<<g, 256, 0, st>>>(ws, ksplit, p.M, p.N, p.ws_ld, c, ldc);
   }
   return check_launch();
 }
@@ -562,35 +585,47 @@ bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
   return macro == 64 || macro == 128 || macro == 256;
 }
 
-int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
-  constexpr int BN = 192;
-  const bool bf = c_dtype == MXQ_BF16;
-  const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM), tiles_n = (int)((b.rows + BN - 1) / BN);
-  const int n_stages = (int)((a.cols + mbs::KSTAGE - 1) / mbs::KSTAGE);
+// Split count for few-tile shapes: split K at stage boundaries so every SM
+// streams weights (decode-like M <= 64 only: at M = 128 the f32 partial
+// traffic and the reduce cost more than the parallelism wins, 18 vs 21 us on
+// the GPT-OSS gate_up shape, profiles/configs_r01.json).
+static int choose_ksplit(int rows_small, int base_clusters, int slots, int n_stages) {
+  if (rows_small > 64 || 2 * base_clusters > slots || n_stages < 4) return 1;
+  int ks = std::min(slots / base_clusters, n_stages / 2);
+  const int spl = (n_stages + ks - 1) / ks;
+  return (n_stages + spl - 1) / spl;  // no empty split
+}
+
+template <int BN, int NB, int EPIW, bool TRANS>
+static int launch_shape(const QDesc& ka, const QDesc& kb, void* c, bool bf, int64_t ldc, int rows_small, cudaStream_t st) {
+  const int tiles_m = (int)((ka.rows + mbs::BM - 1) / mbs::BM), tiles_n = (int)((kb.rows + BN - 1) / BN);
+  const int n_stages = (int)((ka.cols + mbs::KSTAGE - 1) / mbs::KSTAGE);
   // one 128-row block: no pairing across M, so no cluster (its second CTA would idle)
   const int CL = tiles_m >= 2 ? 2 : 1;
-  const int base = ((tiles_m + CL - 1) / CL) * tiles_n;  // clusters' worth of work without splitting K
-  const int slots = num_sms() / CL;
-  // Few tiles and few rows (decode-like M <= 64): split K at stage boundaries
-  // so every SM streams weights.  (At M = 128 the extra f32 partial traffic
-  // and the reduce cost more than the parallelism wins: 18 vs 21 us on the
-  // GPT-OSS gate_up shape, profiles/configs_r01.json.)
-  int ksplit = 1;
-  if (a.rows <= 64 && 2 * base <= slots && n_stages >= 4) {
-    ksplit = std::min(slots / base, n_stages / 2);
-    const int spl = (n_stages + ksplit - 1) / ksplit;
-    ksplit = (n_stages + spl - 1) / spl;  // no empty split
-  }
+  int ksplit = choose_ksplit(rows_small, ((tiles_m + CL - 1) / CL) * tiles_n, num_sms() / CL, n_stages);
   float* ws = nullptr;
   if (ksplit > 1) {
-    ws = mbs::splitk_workspace((size_t)ksplit * a.rows * b.rows * sizeof(float), st);
+    ws = mbs::splitk_workspace((size_t)ksplit * ka.rows * kb.rows * sizeof(float), st);
     if (!ws) ksplit = 1;  // (first use inside a graph capture: run unsplit)
   }
   if (CL == 1)
-    return bf ? mbs::launch<BN, 2, 16, true, 1>(a, b, c, ldc, ksplit, ws, st)
-              : mbs::launch<BN, 2, 16, false, 1>(a, b, c, ldc, ksplit, ws, st);
-  return bf ? mbs::launch<BN, 2, 16, true, 2>(a, b, c, ldc, ksplit, ws, st)
-            : mbs::launch<BN, 2, 16, false, 2>(a, b, c, ldc, ksplit, ws, st);
+    return bf ? mbs::launch<BN, NB, EPIW, true, 1, TRANS>(ka, kb, c, ldc, ksplit, ws, st)
+              : mbs::launch<BN, NB, EPIW, false, 1, TRANS>(ka, kb, c, ldc, ksplit, ws, st);
+  return bf ? mbs::launch<BN, NB, EPIW, true, 2, TRANS>(ka, kb, c, ldc, ksplit, ws, st)
+            : mbs::launch<BN, NB, EPIW, false, 2, TRANS>(ka, kb, c, ldc, ksplit, ws, st);
+}
+
+int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
+  const bool bf = c_dtype == MXQ_BF16;
+  // Decode-sized A (<= 64 rows) against a wide B: swap-AB -- 128 weight rows
+  // per tile on the MMA's M side, the tokens on a narrow N (16-64), four
+  // epilogue warps, transposed stores; the kernel streams weights.
+  if (a.rows <= 64 && b.rows >= 256) {
+    if (a.rows <= 16) return launch_shape<16, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
+    if (a.rows <= 32) return launch_shape<32, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
+    return launch_shape<64, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
+  }
+  return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
 }
 
 }  // namespace mxq

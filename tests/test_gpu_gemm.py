@@ -126,11 +126,13 @@ def test_tc_gemm_mbs_persistent_tiles(va, vb):
     assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
 
 
-@pytest.mark.parametrize("m", [1, 8, 128])
+@pytest.mark.parametrize("m", [1, 8, 33, 64, 128])
 def test_tc_gemm_mbs_small_m_split_k(m):
-    """GPT-OSS expert shapes (config 5): one 128-row block, K = 2880 split across
-    CTAs at stage boundaries (f32 partials summed in a fixed order); the last
-    macro is 64 wide.  Same tolerance as every tcgen05 product, deterministic."""
+    """GPT-OSS expert shapes (config 5): M <= 64 runs swap-AB (weights on the
+    MMA's M side, tokens on N = 16/32/64, transposed stores), K = 2880 split
+    across CTAs at stage boundaries (f32 partials summed in a fixed order); the
+    last macro is 64 wide.  Same tolerance as every tcgen05 product,
+    deterministic."""
     rng = np.random.Generator(np.random.PCG64(31 + m))
     for n in (5760, 2880):
         a = rng.standard_t(4, (m, 2880)).astype(np.float32)
