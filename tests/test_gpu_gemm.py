@@ -145,3 +145,18 @@ def test_tc_gemm_mbs_small_m_split_k(m):
         assert np.array_equal(c, M.matmul_quantized(aq, bq).cpu().numpy())
         cb = M.matmul_quantized(aq, bq, out_dtype=torch.bfloat16).float().cpu().numpy()
         assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
+
+
+@pytest.mark.parametrize("macro", [64, 256])
+def test_tc_gemm_mbs_swap_ab_macro_sizes(macro):
+    """Swap-AB decode path with the other macro widths the kernel takes."""
+    rng = np.random.Generator(np.random.PCG64(71 + macro))
+    m, n, k = 5, 1280, 2048
+    a = rng.standard_t(4, (m, k)).astype(np.float32)
+    b = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+    aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S, macro_size=macro))
+    bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant.MBS_D, macro_size=macro))
+    c = M.matmul_quantized(aq, bq, M.TileConfig(t_k=max(macro, 128))).cpu().numpy()
+    qa, qb = O.quantize(a, "mbs_s", macro_size=macro), O.quantize(b, "mbs_d", macro_size=macro)
+    da, db = O.dequantize(qa).astype(np.float64), O.dequantize(qb).astype(np.float64)
+    _check(c, da @ db.T, np.abs(da) @ np.abs(db).T, ("swap-macro", macro))
