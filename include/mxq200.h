@@ -158,6 +158,21 @@ int mxq_gemm(const mxq_qtensor* a, const mxq_qtensor* b, void* c, int32_t c_dtyp
              void* stream);
 
 /*
+ * Activation quantization fused with the GEMM:
+ * quantize the dense activation x (rows a->rows, cols a->cols, MBS-S with
+ * a->macro_size; the reference runs quantize_tensor src/quantize.py:709-725
+ * then matmul_quantized src/gemm.py:137-172) into `a`, then C = A . B^T.
+ * For bf16 x (32-byte aligned rows) against an MBS/E8M0 B with more than 64
+ * rows of A, both run in ONE launch of the MBS GEMM: every CTA first
+ * quantizes its share of A's 128-row blocks and the GEMM consumes a block as
+ * soon as it is published.  Otherwise the call makes the two launches.  `a`
+ * and C are bit-identical to mxq_quantize followed by mxq_gemm either way.
+ * a must be MBS_S and carry scales_mma and sig_t (scales / mant optional).
+ */
+int mxq_quantize_gemm(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor* a, const mxq_qtensor* b,
+                      void* c, int32_t c_dtype, int64_t ldc, uint32_t* scratch, void* stream);
+
+/*
  * Reference-exact GEMM on CUDA cores: every element is the dequantized f32
  * value, products and sums in f64 with k ascending and no FMA, one final
  * rounding -- bit-identical to matmul_reference(dequantize(a), dequantize(b))

@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libmxq200.so")
 SOURCES = ["capi.cu", "quantize.cu", "qsnr.cu", "layout.cu", "gemm_exact.cu", "gemm_tc.cu", "gemm_mbs.cu"]
-HEADERS = ["mxq_arith.cuh", "mxq_device.cuh", "mxq_internal.h", "tc_ptx.cuh"]
+HEADERS = ["sq_dev.cuh", "mxq_arith.cuh", "mxq_device.cuh", "mxq_internal.h", "tc_ptx.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -99,8 +99,9 @@ int mxq_quantize(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor
   if (!x || !scratch) return set_error(ERR_INVALID, "null input or scratch");
   if (x_dtype != DT_F32 && x_dtype != DT_BF16) return set_error(ERR_INVALID, "x_dtype must be MXQ_F32 or MXQ_BF16");
   if (x_ld < q->cols) return set_error(ERR_INVALID, "x_ld < cols");
-  const int esz = x_dtype == DT_BF16 ? 2 : 4;
-  if (((uintptr_t)x % 16) || ((x_ld * esz) % 16)) return set_error(ERR_UNSUPPORTED, "input must be 16-byte aligned with a 16-byte row pitch");
+  const int esz = x_dtype == DT_BF16 ? 2 : 4, al = x_dtype == DT_BF16 ? 32 : 16;  // (bf16 units are 256-bit loads)
+  if (((uintptr_t)x % al) || ((x_ld * esz) % al))
+    return set_error(ERR_UNSUPPORTED, "input must be aligned with a row pitch of 32 bytes (bf16) / 16 bytes (f32)");
   if (!q->scales && !q->scales_mma) return set_error(ERR_INVALID, "no scale output buffer");
   const bool mbs = q->variant == MBS_S || q->variant == MBS_D;
   if (mbs && !q->mant && !q->sig_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
@@ -175,6 +176,38 @@ int mxq_gemm(const mxq_qtensor* a, const mxq_qtensor* b, void* c, int32_t c_dtyp
   if (a->cols != b->cols) return set_error(ERR_INVALID, "operands disagree on K");
   if (!c || ldc < b->rows) return set_error(ERR_INVALID, "bad output buffer");
   return launch_gemm_tc(*a, *b, c, c_dtype, ldc, scratch, (cudaStream_t)stream);
+}
+
+int mxq_quantize_gemm(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor* a, const mxq_qtensor* b,
+                      void* c, int32_t c_dtype, int64_t ldc, uint32_t* scratch, void* stream) {
+  int rc = validate_q(a, false);
+  if (rc) return rc;
+  rc = validate_q(b, false);
+  if (rc) return rc;
+  if (a->variant != MBS_S) return set_error(ERR_INVALID, "quantize_gemm: the activation side must be MBS_S");
+  if (a->cols != b->cols) return set_error(ERR_INVALID, "operands disagree on K");
+  if (!c || ldc < b->rows) return set_error(ERR_INVALID, "bad output buffer");
+  if (!a->scales_mma || !a->sig_t) return set_error(ERR_INVALID, "quantize_gemm needs A's GEMM layout buffers");
+  const bool fuse = gemm_mbs_fusable(*a, *b, x_dtype) && (((uintptr_t)x | (uintptr_t)(x_ld * 2)) % 32) == 0;
+  if (!fuse) {  // two launches, same results
+    rc = mxq_quantize(x, x_dtype, x_ld, a, 0, nullptr, 0, 0, scratch, stream);
+    if (rc) return rc;
+    return launch_gemm_tc(*a, *b, c, c_dtype, ldc, scratch, (cudaStream_t)stream);
+  }
+  if (!x || !scratch) return set_error(ERR_INVALID, "null input or scratch");
+  if (x_ld < a->cols) return set_error(ERR_INVALID, "x_ld < cols");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t rows_pad = (a->rows + 255) / 256 * 256;
+  if (rows_pad != a->rows || a->sf_kpad != a->cols / a->block_size) {  // padding atoms must hold finite codes
+    cudaError_t e = cudaMemsetAsync(a->scales_mma, 0, (size_t)(rows_pad * a->sf_kpad), st);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
+  if (a->sig_t_ld > a->rows) {
+    const int64_t nmac = (a->cols + a->macro_size - 1) / a->macro_size;
+    cudaError_t e = cudaMemsetAsync(a->sig_t, 0, sizeof(float) * (size_t)(nmac * a->sig_t_ld), st);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
+  return launch_gemm_mbs_fused(x, x_ld, *a, *b, c, c_dtype, ldc, scratch, st);
 }
 
 int mxq_gemm_exact(const mxq_qtensor* a, const mxq_qtensor* b, float* c, int64_t ldc, uint32_t* scratch,

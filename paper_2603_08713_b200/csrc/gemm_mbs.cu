@@ -36,6 +36,7 @@
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
+#include "sq_dev.cuh"
 #include "tc_ptx.cuh"
 
 namespace mxq {
@@ -107,6 +108,15 @@ struct Params {
   int64_t ws_ld;
   uint32_t idesc;
   long long* trace;    // clock64 trace of CTA 0 (MXQ_GEMM_TRACE builds only)
+  // FUSED: the bf16 activation xa (M x K, row pitch xa_ld elements) is
+  // quantized (MBS-S) inside the launch into qa -- the buffers sfa / sga / the
+  // A tensor map point at -- and ready[mb] is set once 128-row block mb is out.
+  const void* xa;
+  int64_t xa_ld;
+  QDesc qa;
+  uint32_t* ready;
+  uint32_t* status;
+  int fused_dbg;       // development timing (MXQ_FUSED_DBG): 1 = quantize only, 2 = GEMM only
 };
 
 #ifndef MXQ_GEMM_TRACE
@@ -159,10 +169,76 @@ __device__ __forceinline__ void reg_fence(float* v) {
                  "+f"(v[i + 6]), "+f"(v[i + 7]));
 }
 
+// Fused MBS-S quantization of A: A's rows are cut into
+// slices of FQ_ROWS rows dealt round-robin to the CTAs (CTA b takes slices b,
+// b + gridDim.x, ...), so all SMs stream the activation; each warp takes
+// 32-unit row segments, four in flight, through the same sq_unit as the
+// standalone k_stream_quant, so codes / scales / mantissas / sigma are
+// bit-identical to mxq_quantize.  A finished slice is published with generic
+// stores -> proxy fence -> CTA barrier -> release add on the slice counter;
+// the TMA warp acquires the full count before its first load.
+constexpr int FQ_ROWS = 8;
+#ifndef MXQ_FQ_U
+#define MXQ_FQ_U 2
+#endif
+template <int G, int THREADS>
+__device__ __forceinline__ void fused_quant_a(const Params& p, const float* sig_tab) {
+  constexpr int NW = THREADS / 32, U = MXQ_FQ_U;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t nblk = (uint32_t)p.K / 16, segs = (nblk + 31) / 32;
+  const uint32_t nslices = (uint32_t)(p.M + FQ_ROWS - 1) / FQ_ROWS;
+  const uint32_t my_slices = nslices > blockIdx.x ? (nslices - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+  // this CTA's segments, flattened over its slices (one latency round per
+  // U segments per warp, no barrier between slices)
+  const uint32_t per_slice = FQ_ROWS * segs, nseg = my_slices * per_slice;
+  uint32_t bad = 0, ovf = 0;
+  for (uint32_t s0 = warp; s0 < nseg; s0 += U * NW) {
+    Blk16<DT_BF16> xb[U];
+    uint32_t rr[U], kk[U];
+    bool live[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t j = s0 + u * NW;
+      const uint32_t js = j / per_slice, jr = j - js * per_slice;
+      const uint32_t rl = jr / segs;
+      rr[u] = (blockIdx.x + js * gridDim.x) * FQ_ROWS + rl;
+      kk[u] = (jr - rl * segs) * 32 + lane;
+      live[u] = j < nseg && rr[u] < (uint32_t)p.M;
+      if (live[u] && kk[u] < nblk) ld_blk<DT_BF16>(p.xa, (int64_t)rr[u] * p.xa_ld + kk[u] * 16, xb[u]);
+      else zero_blk<DT_BF16>(xb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (live[u])
+        sq_unit<DT_BF16, SQ_MBS_S, G>(xb[u], kk[u] < nblk, row_out(p.qa, rr[u]), p.qa.sig_t_ld, kk[u], lane,
+                                      sig_tab, bad, ovf);
+  }
+  if (bad) atomicOr(p.status, ST_NONFINITE);
+  if (ovf) atomicOr(p.status, ST_OVERFLOW);
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0 && my_slices) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.ready + (p.M + BM - 1) / BM), "r"(my_slices)
+                 : "memory");
+  }
+}
+
+__device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t want) {
+  uint32_t v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (v >= want) break;
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // TRANS: swap-AB for decode-sized M -- the kernel's A operand is the weight
 // matrix (128 weight rows per tile) and its B operand the few activation rows
 // (BN >= M), so the output tile is stored transposed into C[token][n].
-template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS>
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
 __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
     k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
   using C = MbsCfg<BN_, NB_, EPIW_>;
@@ -179,6 +255,20 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
   const uint32_t a_tfull = a_empty + 8 * STAGES, a_tempty = a_tfull + 8 * NB;
   const uint32_t a_sfull = a_tempty + 8 * NB, a_sempty = a_sfull + 8 * NSIG;
   const uint32_t a_tmem_slot = a_sempty + 8 * NSIG;
+
+  if constexpr (FUSED) if (p.fused_dbg != 2) {
+    // phase 1: quantize this CTA's A row blocks (sigma table in the sigma ring's space)
+    float* sig_tab = reinterpret_cast<float*>(smem_raw + (a_smem - smem_u32(smem_raw)) + OFF_SIG);
+    for (int i = threadIdx.x; i < 256; i += C::THREADS) sig_tab[i] = 1.0f / mbs_factor((uint32_t)i);
+    __syncthreads();
+    if (p.mac_steps == 1) fused_quant_a<4, C::THREADS>(p, sig_tab);
+    else if (p.mac_steps == 2) fused_quant_a<8, C::THREADS>(p, sig_tab);
+    else fused_quant_a<16, C::THREADS>(p, sig_tab);
+    // (the sigma ring is rewritten by bulk copies: order the generic writes first)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (p.fused_dbg == 1) return;
+  }
 
   // warp index through a shuffle so ptxas knows it is warp-uniform
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -241,6 +331,11 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
     if constexpr (C::SETMAXNREG) setmaxnreg_dec<C::CTRL_REGS>();
     if (warp == W_TMA) {
       // ===================== TMA producer =====================
+      // (fused: A is complete once every slice is published -- the first wave
+      // of tiles covers every row block, so one wait before the loop costs
+      // nothing and keeps the 32-register producer loop free of spills)
+      if constexpr (FUSED)
+        if (p.fused_dbg != 2) wait_ready(p.ready + (p.M + BM - 1) / BM, (uint32_t)((p.M + FQ_ROWS - 1) / FQ_ROWS));
       uint32_t st = 0, ph = 0, slot = 0, sph = 0;
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         const Unit U = unit_of(unit);
@@ -503,11 +598,12 @@ static float* splitk_workspace(size_t bytes, cudaStream_t st) {
   return ptr[dev];
 }
 
-template <int BN, int NB, int EPIW, bool OUT_BF16, int CL, bool TRANS>
-static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int ksplit, float* ws, cudaStream_t st) {
+template <int BN, int NB, int EPIW, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
+static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int ksplit, float* ws, cudaStream_t st,
+                  const void* xa = nullptr, int64_t xa_ld = 0, uint32_t* ready = nullptr, uint32_t* status = nullptr) {
   using C = MbsCfg<BN, NB, EPIW>;
   constexpr int SMEM = C::SMEM;
-  auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL, TRANS>;
+  auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL, TRANS, FUSED>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
@@ -544,6 +640,19 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   p.ws = ws;
   p.ws_ld = TRANS ? p.M : p.N;
   p.trace = g_trace;
+  p.xa = xa;
+  p.xa_ld = xa_ld;
+  p.qa = a;
+  p.ready = ready;
+  p.status = status;
+  if constexpr (FUSED) {
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* d = getenv("MXQ_FUSED_DBG");
+      dbg = d ? atoi(d) : 0;
+    }
+    p.fused_dbg = dbg;
+  }
   // E2M1 x E2M1, UE8M0 scales, N = BN, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
   p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
   const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN) * ksplit;
@@ -626,6 +735,50 @@ int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_
     return launch_shape<64, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
   }
   return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
+}
+
+// Per-device ready flags of the fused launch (one per 128-row block of A).
+static uint32_t* ready_flags(int64_t n, cudaStream_t st) {
+  static uint32_t* ptr[64] = {nullptr};
+  static int64_t cap[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (cap[dev] < n) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    if (ptr[dev]) {
+      cudaStreamSynchronize(st);
+      cudaFree(ptr[dev]);
+    }
+    ptr[dev] = nullptr;
+    cap[dev] = 0;
+    const int64_t want = std::max<int64_t>(n, 1024);
+    if (cudaMalloc(&ptr[dev], want * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    cap[dev] = want;
+  }
+  if (cudaMemsetAsync(ptr[dev], 0, n * sizeof(uint32_t), st) != cudaSuccess) return nullptr;
+  return ptr[dev];
+}
+
+bool gemm_mbs_fusable(const QDesc& a, const QDesc& b, int x_dtype) {
+  return x_dtype == DT_BF16 && a.variant == MBS_S && gemm_mbs_supported(a, b) && !(a.rows <= 64 && b.rows >= 256) &&
+         a.scales_mma && a.sig_t;
+}
+
+// Fused MBS-S activation quantization + MBS GEMM in one launch (callers check
+// gemm_mbs_fusable first; x is bf16 with a 32-byte aligned row pitch).
+int launch_gemm_mbs_fused(const void* x, int64_t x_ld, const QDesc& a, const QDesc& b, void* c, int c_dtype,
+                          int64_t ldc, uint32_t* status, cudaStream_t st) {
+  const bool bf = c_dtype == MXQ_BF16;
+  const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM);
+  uint32_t* ready = ready_flags(tiles_m + 1, st);  // (the slice counter is ready[tiles_m])
+  if (!ready) return set_error(ERR_UNSUPPORTED, "fused quantize+GEMM: no ready-flag buffer (first use inside a graph capture)");
+  if (tiles_m >= 2)
+    return bf ? mbs::launch<192, 2, 16, true, 2, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status)
+              : mbs::launch<192, 2, 16, false, 2, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status);
+  return bf ? mbs::launch<192, 2, 16, true, 1, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status)
+            : mbs::launch<192, 2, 16, false, 1, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status);
 }
 
 }  // namespace mxq

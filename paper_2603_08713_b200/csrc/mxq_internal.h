@@ -31,6 +31,9 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
                    cudaStream_t st);
 bool gemm_mbs_supported(const QDesc& a, const QDesc& b);
 int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st);
+bool gemm_mbs_fusable(const QDesc& a, const QDesc& b, int x_dtype);
+int launch_gemm_mbs_fused(const void* x, int64_t x_ld, const QDesc& a, const QDesc& b, void* c, int c_dtype,
+                          int64_t ldc, uint32_t* status, cudaStream_t st);
 void set_gemm_trace(long long* p);
 int launch_build_gemm_layout(const QDesc& q, int sf_block, cudaStream_t st);
 

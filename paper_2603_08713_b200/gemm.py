@@ -19,10 +19,10 @@ import numpy as np
 import torch
 
 from . import _lib
-from .quantize import QuantizedTensor, Variant
+from .quantize import QuantizedTensor, SchemeConfig, Variant, quantize_tensor
 
-__all__ = ["TileConfig", "OverheadReport", "matmul_reference", "matmul_quantized", "roofline_overhead",
-           "max_ulp_divergence", "tc_supported"]
+__all__ = ["TileConfig", "OverheadReport", "matmul_reference", "matmul_quantized", "quantize_matmul",
+           "roofline_overhead", "max_ulp_divergence", "tc_supported"]
 
 
 @dataclass(frozen=True)
@@ -128,6 +128,54 @@ def matmul_quantized(aq: QuantizedTensor, bq: QuantizedTensor, cfg: TileConfig =
     _lib.check(L.mxq_gemm(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), dt, c.stride(0), status.data_ptr(),
                           stream), "matmul_quantized")
     return c
+
+
+def quantize_matmul(a, bq: QuantizedTensor, cfg: SchemeConfig = SchemeConfig(Variant.MBS_S),
+                    tile: TileConfig = TileConfig(), *, out_dtype: torch.dtype = torch.float32,
+                    out: torch.Tensor = None, check: bool = True):
+    """``(matmul_quantized(aq, bq), aq)`` with ``aq = quantize_tensor(a, cfg)``
+    (src/quantize.py:709-725, src/gemm.py:137-172) -- the activation side of
+    a quantized linear layer.
+
+    For an MBS-S activation (bf16, more than 64 rows) against an MBS / E8M0
+    weight, the quantization runs inside the GEMM launch (csrc/gemm_mbs.cu,
+    ``fused_quant_a``): each CTA quantizes its share of A's 128-row blocks and
+    the GEMM consumes a block as soon as it is published, so there is no
+    separate quantizer launch.  Every other case makes the two calls.  The
+    result and ``aq`` are bit-identical either way.
+    """
+    from . import quantize as _q
+
+    cfg = cfg if isinstance(cfg, SchemeConfig) else SchemeConfig(cfg)
+    fusable = (cfg.variant is Variant.MBS_S and bq.variant in (Variant.MBS_S, Variant.MBS_D, Variant.MX16,
+                                                                Variant.MX16_OAS, Variant.OCP32)
+               and isinstance(a, torch.Tensor) and a.dtype == torch.bfloat16 and a.is_cuda)
+    if not fusable:
+        aq = quantize_tensor(a, cfg, check=check)
+        return matmul_quantized(aq, bq, tile, out_dtype=out_dtype, out=out, check=check), aq
+    x, dt = _q._as_device_2d(a, 16)
+    rows, cols = x.shape
+    if cols != bq.shape[1]:
+        raise ValueError(f"operands disagree on K: {(rows, cols)} vs {bq.shape}")
+    macro = cfg.macro_size
+    if tile.t_k % 16 != 0:  # _validate_chunking for the operand not yet quantized
+        raise ValueError(f"t_k {tile.t_k} is not a multiple of operand a's block size 16")
+    if tile.t_k % macro != 0:
+        raise ValueError(f"t_k {tile.t_k} is not a multiple of operand a's macro size {macro}")
+    _validate_chunking(bq, tile.t_k, "b")
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("out_dtype must be float32 or bfloat16")
+    bufs = _q._Outputs(Variant.MBS_S, rows, cols, 16, macro, x.device, True)
+    qa = bufs.qt(Variant.MBS_S, rows, cols, 16, macro)
+    n = bq.shape[0]
+    c = out if out is not None else torch.empty((rows, n), dtype=out_dtype, device=x.device)
+    qb = bq.gemm_qt(16)  # (an MBS-S A makes the pair block-16)
+    dtc = _lib.MXQ_BF16 if out_dtype == torch.bfloat16 else _lib.MXQ_F32
+    _lib.check(_lib.lib().mxq_quantize_gemm(x.data_ptr(), dt, x.stride(0), ctypes.byref(qa), ctypes.byref(qb),
+                                            c.data_ptr(), dtc, c.stride(0), bufs.status.data_ptr(),
+                                            _lib.stream_handle()), "quantize_matmul")
+    aq = _q._result(bufs, Variant.MBS_S, rows, cols, 16, macro, check)
+    return c, aq
 
 
 def roofline_overhead(cfg: TileConfig, sigma_bytes: int = 2, out_bytes: int = 4) -> OverheadReport:

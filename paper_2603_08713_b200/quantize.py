@@ -442,10 +442,11 @@ def _as_device_2d(t, bs: int):
     if x.device != dev:
         x = x.to(dev, non_blocking=True)
     esz = x.element_size()
-    if x.stride(1) != 1 or (x.stride(0) * esz) % 16 or x.data_ptr() % 16:
+    # the streaming kernels read 32-byte units: 32-byte aligned base and row pitch
+    if x.stride(1) != 1 or (x.stride(0) * esz) % 32 or x.data_ptr() % 32:
         x = x.contiguous()
-        if (x.stride(0) * esz) % 16:
-            pitch = _round_up(x.shape[1], 16 // esz)
+        if (x.stride(0) * esz) % 32 or x.data_ptr() % 32:
+            pitch = _round_up(x.shape[1], 32 // esz)
             buf = torch.empty((x.shape[0], pitch), dtype=x.dtype, device=dev)
             buf[:, : x.shape[1]] = x
             x = buf[:, : x.shape[1]]
@@ -520,7 +521,14 @@ def quantize_tensor(t, cfg: SchemeConfig, *, check: bool = True, gemm_layout: bo
         rc = L.mxq_quantize(x.data_ptr(), dt, x.stride(0), ctypes.byref(q), 0, cand.ctypes.data, len(cand),
                             int(cfg.augment_static), out.status.data_ptr(), stream)
     _lib.check(rc, "quantize_tensor")
-    nv = cfg.variant is Variant.NVFP4
+    return _result(out, cfg.variant, rows, cols, bs, macro, check)
+
+
+def _result(out: "_Outputs", variant: Variant, rows: int, cols: int, bs: int, macro: int,
+            check: bool) -> QuantizedTensor:
+    """QuantizedTensor over the buffers a quantize call wrote (the status word
+    is checked now with ``check``, else kept for ``_raise_status``)."""
+    nv = variant is Variant.NVFP4
     ts: Any = None
     if check:
         _lib.raise_on_status(out.status)
@@ -529,7 +537,7 @@ def quantize_tensor(t, cfg: SchemeConfig, *, check: bool = True, gemm_layout: bo
     elif nv:
         ts = out.ts
     res = QuantizedTensor(
-        variant=cfg.variant, shape=(rows, cols), block_size=bs, macro_size=macro, codes=out.codes,
+        variant=variant, shape=(rows, cols), block_size=bs, macro_size=macro, codes=out.codes,
         block_scales=None if nv else out.scales, e4m3_scales=out.scales if nv else None,
         mbs_mantissas=out.mant, tensor_scale=ts)
     c = res._cache

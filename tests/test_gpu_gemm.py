@@ -160,3 +160,51 @@ def test_tc_gemm_mbs_swap_ab_macro_sizes(macro):
     qa, qb = O.quantize(a, "mbs_s", macro_size=macro), O.quantize(b, "mbs_d", macro_size=macro)
     da, db = O.dequantize(qa).astype(np.float64), O.dequantize(qb).astype(np.float64)
     _check(c, da @ db.T, np.abs(da) @ np.abs(db).T, ("swap-macro", macro))
+
+
+# ---------------------------------------------------------------------------
+# activation quantization fused into the MBS GEMM launch.
+# The fused result must be bit-identical to quantize_tensor + matmul_quantized.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("m,n,k,macro,wv,out_dtype", [
+    (256, 768, 1024, 128, "mbs_d", torch.float32),
+    (200, 1280, 2880, 128, "mbs_d", torch.bfloat16),   # partial row block, partial last macro (64) and stage
+    (1000, 1536, 4096, 64, "mbs_s", torch.float32),
+    (384, 576, 2048, 256, "mbs_d", torch.bfloat16),
+    (130, 640, 1024, 128, "mx16_oas", torch.float32),  # non-MBS weight side
+    (48, 1024, 1024, 128, "mbs_d", torch.float32),     # decode size: two launches (swap-AB GEMM)
+])
+def test_quantize_matmul_fused_matches_two_step(m, n, k, macro, wv, out_dtype):
+    g = torch.Generator(device="cuda").manual_seed(1000 + m + k)
+    a = (torch.randn(m, k, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    w = (torch.randn(n, k, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    wvar = M.Variant(wv)
+    wcfg = M.SchemeConfig(wvar, macro_size=macro) if wvar in (M.Variant.MBS_S, M.Variant.MBS_D) else M.SchemeConfig(wvar)
+    wq = M.quantize_tensor(w, wcfg)
+    acfg = M.SchemeConfig(M.Variant.MBS_S, macro_size=macro)
+    tile = M.TileConfig(t_k=max(macro, 128))
+    c_f, aq_f = M.quantize_matmul(a, wq, acfg, tile, out_dtype=out_dtype)
+    aq_2 = M.quantize_tensor(a, acfg)
+    c_2 = M.matmul_quantized(aq_2, wq, tile, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    assert aq_f == aq_2
+    assert torch.equal(aq_f._cache["sig_t"][:, :m], aq_2._cache["sig_t"][:, :m])
+    assert torch.equal(c_f, c_2)
+
+
+def test_quantize_matmul_fused_repeated_and_nonfinite():
+    """Back-to-back fused launches (ready flags reset per launch) and the
+    non-finite check of the fused quantizer."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    w = (torch.randn(1536, 2048, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    wq = M.quantize_tensor(w, M.SchemeConfig(M.Variant.MBS_D))
+    xs = [torch.randn(512, 2048, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3)]
+    ref = [M.matmul_quantized(M.quantize_tensor(x, M.SchemeConfig(M.Variant.MBS_S)), wq) for x in xs]
+    for _ in range(2):
+        for x, r in zip(xs, ref):
+            c, _ = M.quantize_matmul(x, wq)
+            assert torch.equal(c, r)
+    bad = xs[0].clone()
+    bad[300, 7] = float("nan")
+    with pytest.raises(ValueError):
+        M.quantize_matmul(bad, wq)
