@@ -168,6 +168,8 @@ int mxq_gemm(const mxq_qtensor* a, const mxq_qtensor* b, void* c, int32_t c_dtyp
  * soon as it is published.  Otherwise the call makes the two launches.  `a`
  * and C are bit-identical to mxq_quantize followed by mxq_gemm either way.
  * a must be MBS_S and carry scales_mma and sig_t (scales / mant optional).
+ * scratch: device u32[4] as for mxq_quantize; scratch[2] is the launch's
+ * published-slice counter (zeroed by the call).
  */
 int mxq_quantize_gemm(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor* a, const mxq_qtensor* b,
                       void* c, int32_t c_dtype, int64_t ldc, uint32_t* scratch, void* stream);

@@ -114,7 +114,7 @@ struct Params {
   const void* xa;
   int64_t xa_ld;
   QDesc qa;
-  uint32_t* ready;
+  uint32_t* ready;     // slices published (zeroed before the launch)
   uint32_t* status;
   int fused_dbg;       // development timing (MXQ_FUSED_DBG): 1 = quantize only, 2 = GEMM only
 };
@@ -220,7 +220,7 @@ __device__ __forceinline__ void fused_quant_a(const Params& p, const float* sig_
   __syncthreads();
   if (threadIdx.x == 0 && my_slices) {
     __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.ready + (p.M + BM - 1) / BM), "r"(my_slices)
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.ready), "r"(my_slices)
                  : "memory");
   }
 }
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
       // of tiles covers every row block, so one wait before the loop costs
       // nothing and keeps the 32-register producer loop free of spills)
       if constexpr (FUSED)
-        if (p.fused_dbg != 2) wait_ready(p.ready + (p.M + BM - 1) / BM, (uint32_t)((p.M + FQ_ROWS - 1) / FQ_ROWS));
+        if (p.fused_dbg != 2) wait_ready(p.ready, (uint32_t)((p.M + FQ_ROWS - 1) / FQ_ROWS));
       uint32_t st = 0, ph = 0, slot = 0, sph = 0;
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         const Unit U = unit_of(unit);
@@ -577,39 +577,14 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const float* __restrict__
   }
 }
 
-// Per-device f32 workspace for split-K partials, grown outside graph capture.
-static float* splitk_workspace(size_t bytes, cudaStream_t st) {
-  static float* ptr[64] = {nullptr};
-  static size_t cap[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (cap[dev] >= bytes) return ptr[dev];
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-  if (ptr[dev]) {
-    cudaStreamSynchronize(st);
-    cudaFree(ptr[dev]);
-  }
-  ptr[dev] = nullptr;
-  cap[dev] = 0;
-  if (cudaMalloc(&ptr[dev], bytes) != cudaSuccess) return nullptr;
-  cap[dev] = bytes;
-  return ptr[dev];
-}
-
 template <int BN, int NB, int EPIW, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
 static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int ksplit, float* ws, cudaStream_t st,
                   const void* xa = nullptr, int64_t xa_ld = 0, uint32_t* ready = nullptr, uint32_t* status = nullptr) {
   using C = MbsCfg<BN, NB, EPIW>;
   constexpr int SMEM = C::SMEM;
   auto kern = k_gemm_mbs<BN, NB, EPIW, OUT_BF16, CL, TRANS, FUSED>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e);
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_set{0};
+  if (const int rc0 = smem_attr_once(kern, SMEM, attr_set)) return rc0;
   CUtensorMap ta, tb;
   int rc = make_code_map(&ta, a.codes, a.rows, a.cols / 2, a.codes_ld, BM);
   if (rc) return rc;
@@ -712,16 +687,29 @@ static int launch_shape(const QDesc& ka, const QDesc& kb, void* c, bool bf, int6
   // one 128-row block: no pairing across M, so no cluster (its second CTA would idle)
   const int CL = tiles_m >= 2 ? 2 : 1;
   int ksplit = choose_ksplit(rows_small, ((tiles_m + CL - 1) / CL) * tiles_n, num_sms() / CL, n_stages);
+  // split-K partials: a stream-ordered allocation per call (pool-cached,
+  // graph-capturable, private to this launch -- no workspace shared between
+  // streams); without one the launch runs unsplit
   float* ws = nullptr;
-  if (ksplit > 1) {
-    ws = mbs::splitk_workspace((size_t)ksplit * ka.rows * kb.rows * sizeof(float), st);
-    if (!ws) ksplit = 1;  // (first use inside a graph capture: run unsplit)
+  if (ksplit > 1 &&
+      cudaMallocAsync(reinterpret_cast<void**>(&ws), (size_t)ksplit * ka.rows * kb.rows * sizeof(float), st) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    ws = nullptr;
+    ksplit = 1;
   }
+  int rc;
   if (CL == 1)
-    return bf ? mbs::launch<BN, NB, EPIW, true, 1, TRANS>(ka, kb, c, ldc, ksplit, ws, st)
-              : mbs::launch<BN, NB, EPIW, false, 1, TRANS>(ka, kb, c, ldc, ksplit, ws, st);
-  return bf ? mbs::launch<BN, NB, EPIW, true, 2, TRANS>(ka, kb, c, ldc, ksplit, ws, st)
+    rc = bf ? mbs::launch<BN, NB, EPIW, true, 1, TRANS>(ka, kb, c, ldc, ksplit, ws, st)
+            : mbs::launch<BN, NB, EPIW, false, 1, TRANS>(ka, kb, c, ldc, ksplit, ws, st);
+  else
+    rc = bf ? mbs::launch<BN, NB, EPIW, true, 2, TRANS>(ka, kb, c, ldc, ksplit, ws, st)
             : mbs::launch<BN, NB, EPIW, false, 2, TRANS>(ka, kb, c, ldc, ksplit, ws, st);
+  if (ws) {
+    const cudaError_t e = cudaFreeAsync(ws, st);
+    if (!rc && e != cudaSuccess) return set_cuda_error(e);
+  }
+  return rc;
 }
 
 int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st) {
@@ -737,30 +725,6 @@ int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_
   return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
 }
 
-// Per-device ready flags of the fused launch (one per 128-row block of A).
-static uint32_t* ready_flags(int64_t n, cudaStream_t st) {
-  static uint32_t* ptr[64] = {nullptr};
-  static int64_t cap[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return nullptr;
-  if (cap[dev] < n) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-    if (ptr[dev]) {
-      cudaStreamSynchronize(st);
-      cudaFree(ptr[dev]);
-    }
-    ptr[dev] = nullptr;
-    cap[dev] = 0;
-    const int64_t want = std::max<int64_t>(n, 1024);
-    if (cudaMalloc(&ptr[dev], want * sizeof(uint32_t)) != cudaSuccess) return nullptr;
-    cap[dev] = want;
-  }
-  if (cudaMemsetAsync(ptr[dev], 0, n * sizeof(uint32_t), st) != cudaSuccess) return nullptr;
-  return ptr[dev];
-}
-
 bool gemm_mbs_fusable(const QDesc& a, const QDesc& b, int x_dtype) {
   return x_dtype == DT_BF16 && a.variant == MBS_S && gemm_mbs_supported(a, b) && !(a.rows <= 64 && b.rows >= 256) &&
          a.scales_mma && a.sig_t;
@@ -772,8 +736,9 @@ int launch_gemm_mbs_fused(const void* x, int64_t x_ld, const QDesc& a, const QDe
                           int64_t ldc, uint32_t* status, cudaStream_t st) {
   const bool bf = c_dtype == MXQ_BF16;
   const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM);
-  uint32_t* ready = ready_flags(tiles_m + 1, st);  // (the slice counter is ready[tiles_m])
-  if (!ready) return set_error(ERR_UNSUPPORTED, "fused quantize+GEMM: no ready-flag buffer (first use inside a graph capture)");
+  uint32_t* ready = status + 2;  // the call's own scratch word: nothing shared between launches
+  const cudaError_t e = cudaMemsetAsync(ready, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return set_cuda_error(e);
   if (tiles_m >= 2)
     return bf ? mbs::launch<192, 2, 16, true, 2, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status)
               : mbs::launch<192, 2, 16, false, 2, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status);

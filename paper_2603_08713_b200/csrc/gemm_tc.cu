@@ -682,12 +682,8 @@ template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL
 static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, bool ue8m0, cudaStream_t st) {
   using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
   auto kern = k_gemm_tc<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return set_cuda_error(e);
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_set{0};
+  if (const int rc0 = smem_attr_once(kern, C::SMEM, attr_set)) return rc0;
   CUtensorMap ta, tb;
   int rc = make_code_map(&ta, a.codes, a.rows, a.cols / 2, a.codes_ld, BM);
   if (rc) return rc;

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/mxq200.h"
 
 namespace mxq {
@@ -14,6 +16,20 @@ enum { ERR_INVALID = MXQ_ERR_INVALID, ERR_UNSUPPORTED = MXQ_ERR_UNSUPPORTED };
 
 int set_error(int code, const char* msg);
 int set_cuda_error(cudaError_t e);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device):
+// `done` is the caller's per-kernel static, one bit per device ordinal.
+template <typename K>
+inline int smem_attr_once(K kern, int smem, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return 0;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  done.fetch_or(bit, std::memory_order_release);
+  return 0;
+}
 int check_launch();
 int num_sms();
 
