@@ -269,3 +269,20 @@ def test_streaming_quantizer_ragged_rows_match_oracle(variant):
         assert np.array_equal(sc, o.block_scales if o.block_scales is not None else o.e4m3_scales)
         if o.mbs_mantissas is not None:
             assert np.array_equal(_np(q.mbs_mantissas), o.mbs_mantissas)
+
+
+@pytest.mark.parametrize("variant", ["mx16_oas", "mbs_s", "nvfp4"])
+def test_strided_bf16_views_quantize_like_contiguous(variant):
+    """bf16 views whose base or row pitch is not 32-byte aligned (the 256-bit
+    unit loads need it) are staged by the wrapper and give the same bits as a
+    contiguous copy; aligned strided views are read in place."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    big = torch.randn(70, 1040, device="cuda", generator=g).to(torch.bfloat16)
+    cfg = M.SchemeConfig(M.Variant(variant))
+    views = [big[:, 8:1032],      # base offset 16 B: misaligned
+             big[1:, 16:1040],    # pitch 2080 B (32-aligned), base +2112 B
+             big[::2, :1024]]     # pitch 4160 B
+    for v in views:
+        qa = M.quantize_tensor(v, cfg)
+        qb = M.quantize_tensor(v.contiguous(), cfg)
+        assert qa == qb, (variant, v.stride(), v.data_ptr() % 32)
