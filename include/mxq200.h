@@ -158,6 +158,19 @@ int mxq_gemm(const mxq_qtensor* a, const mxq_qtensor* b, void* c, int32_t c_dtyp
              void* stream);
 
 /*
+ * Grouped decode GEMMs (MoE experts; SURVEY section 8 d config 5): the n
+ * independent products C_g = A_g . B_g^T (matmul_quantized src/gemm.py:137-172
+ * per group), A_g the tokens routed to expert g (<= 64 rows), B_g the
+ * expert's weights, every B_g of one shape.  a, b: HOST arrays of n
+ * descriptors; c: HOST array of n device output pointers (row stride ldc).
+ * When the pairs are MBS / E8M0 pairs of one variant pair and macro size, all
+ * groups run in one launch of the swap-AB MBS kernel per 64 groups; otherwise
+ * one mxq_gemm launch per group.  Same tolerance parity as mxq_gemm.
+ */
+int mxq_gemm_grouped(const mxq_qtensor* a, const mxq_qtensor* b, int32_t n, void* const* c, int32_t c_dtype,
+                     int64_t ldc, uint32_t* scratch, void* stream);
+
+/*
  * Activation quantization fused with the GEMM:
  * quantize the dense activation x (rows a->rows, cols a->cols, MBS-S with
  * a->macro_size; the reference runs quantize_tensor src/quantize.py:709-725

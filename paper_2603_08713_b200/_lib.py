@@ -56,6 +56,7 @@ SIGNATURES = {
     "mxq_qsnr": (ctypes.c_int, [_P, _I32, _I64, _PQT, _P, _I64, _I64, _I64, _P, _P, _P, _P]),
     "mxq_gemm": (ctypes.c_int, [_PQT, _PQT, _P, _I32, _I64, _P, _P]),
     "mxq_quantize_gemm": (ctypes.c_int, [_P, _I32, _I64, _PQT, _PQT, _P, _I32, _I64, _P, _P]),
+    "mxq_gemm_grouped": (ctypes.c_int, [_PQT, _PQT, _I32, _P, _I32, _I64, _P, _P]),
     "mxq_gemm_exact": (ctypes.c_int, [_PQT, _PQT, _P, _I64, _P, _P]),
     "mxq_matmul_reference": (ctypes.c_int, [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _I64, _P]),
     "mxq_build_gemm_layout": (ctypes.c_int, [_PQT, _I32, _P]),

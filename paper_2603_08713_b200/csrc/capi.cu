@@ -210,6 +210,26 @@ int mxq_quantize_gemm(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qt
   return launch_gemm_mbs_fused(x, x_ld, *a, *b, c, c_dtype, ldc, scratch, st);
 }
 
+int mxq_gemm_grouped(const mxq_qtensor* a, const mxq_qtensor* b, int32_t n, void* const* c, int32_t c_dtype,
+                     int64_t ldc, uint32_t* scratch, void* stream) {
+  if (!a || !b || !c || n < 1) return set_error(ERR_INVALID, "bad group arrays");
+  for (int g = 0; g < n; ++g) {
+    int rc = validate_q(&a[g], false);
+    if (rc) return rc;
+    rc = validate_q(&b[g], false);
+    if (rc) return rc;
+    if (a[g].cols != b[g].cols) return set_error(ERR_INVALID, "operands disagree on K");
+    if (!c[g] || ldc < b[g].rows) return set_error(ERR_INVALID, "bad output buffer");
+  }
+  const int rc = launch_gemm_mbs_grouped(a, b, n, c, c_dtype, ldc, (cudaStream_t)stream);
+  if (rc != ERR_UNSUPPORTED) return rc;
+  for (int g = 0; g < n; ++g) {  // groups the grouped kernel does not take: one launch each
+    const int r = launch_gemm_tc(a[g], b[g], c[g], c_dtype, ldc, scratch, (cudaStream_t)stream);
+    if (r) return r;
+  }
+  return 0;
+}
+
 int mxq_gemm_exact(const mxq_qtensor* a, const mxq_qtensor* b, float* c, int64_t ldc, uint32_t* scratch,
                    void* stream) {
   int rc = validate_q(a, true);

@@ -33,6 +33,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cstring>
+#include <memory>
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
@@ -117,6 +119,29 @@ struct Params {
   uint32_t* ready;     // slices published (zeroed before the launch)
   uint32_t* status;
   int fused_dbg;       // development timing (MXQ_FUSED_DBG): 1 = quantize only, 2 = GEMM only
+};
+
+// Grouped launch (GPT-OSS-style expert GEMMs, SURVEY section 8 d config 5): up
+// to MAXG independent decode-sized GEMMs of one shape in ONE launch, swap-AB
+// form (weights on the MMA's M side).  Per group: the two tensor maps and the
+// operand / output pointers; everything else is shared (GroupTable::p).  The
+// table travels as a __grid_constant__ kernel parameter (param space, no
+// device allocation, graph-capturable).
+constexpr int MAXG = 64;
+struct GroupDesc {
+  CUtensorMap tmA, tmB;  // weights (kernel A), tokens (kernel B)
+  const uint8_t* sfa;
+  const uint8_t* sfb;
+  const float* sga;
+  const float* sgb;
+  int64_t sgb_ld;
+  void* c;
+  int n;                 // tokens of this group (kernel N)
+};
+struct GroupTable {
+  Params p;
+  int n_groups;
+  GroupDesc g[MAXG];
 };
 
 #ifndef MXQ_GEMM_TRACE
@@ -238,9 +263,9 @@ __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t want) 
 // TRANS: swap-AB for decode-sized M -- the kernel's A operand is the weight
 // matrix (128 weight rows per tile) and its B operand the few activation rows
 // (BN >= M), so the output tile is stored transposed into C[token][n].
-template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
-__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
-    k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS, bool FUSED, bool GROUPED>
+__device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorMap* tmB, const Params& p,
+                                         const GroupTable* gt) {
   using C = MbsCfg<BN_, NB_, EPIW_>;
   constexpr int EPIW = C::EPIW, W_TMA = C::W_TMA, W_MMA = C::W_MMA;
   constexpr int BN = C::BN, NB = C::NB, STAGES = C::STAGES, COLS = C::COLS, NRB = C::NRB;
@@ -275,7 +300,8 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
   const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
   const int groups_m = (tiles_m + CL - 1) / CL;
   const int ksplit = p.ksplit;
-  const int num_units = groups_m * tiles_n * ksplit;
+  const int upg = groups_m * tiles_n * ksplit;  // units per group
+  const int num_units = GROUPED ? gt->n_groups * upg : upg;
   const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
   uint32_t crank = 0;
   if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
@@ -286,9 +312,11 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
   const int spl = (n_stages + ksplit - 1) / ksplit;         // stages per K split
   // A work unit: one (128-row group, BN-column tile, K split) of the output;
   // the CTAs of a cluster take consecutive 128-row blocks of it.
-  struct Unit { int mb, nb, split, s_lo, s_hi, c_lo, c_hi; };
+  struct Unit { int g, mb, nb, split, s_lo, s_hi, c_lo, c_hi; };
   auto unit_of = [&](int u) {
     Unit r;
+    r.g = GROUPED ? u / upg : 0;
+    u -= r.g * upg;
     r.split = u % ksplit;
     const int rest = u / ksplit;
     r.mb = (rest % groups_m) * CL + (int)crank;
@@ -314,8 +342,10 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
       mbar_init_a(a_sempty + 8 * b, EPIW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if constexpr (!GROUPED) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmB)) : "memory");
+    }
   }
   if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(a_tmem_slot) : "memory");
@@ -343,22 +373,39 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
         const int rb0 = n0 / 128;
         const int nrb = (rb0 + NRB <= p.sfb_rb) ? NRB : p.sfb_rb - rb0;
         const uint32_t tx = STAGE_A + STAGE_B + SFA_BYTES + nrb * 4 * ATOM;
-        const uint8_t* sa = p.sfa + (int64_t)U.mb * p.sfa_kg * ATOM;
-        const uint8_t* sb = p.sfb + (int64_t)rb0 * p.sfb_kg * ATOM;
-        const float* ga = p.sga + (p.sga_ld ? m0 : 0);
-        const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
+        const CUtensorMap* mA = tmA;
+        const CUtensorMap* mB = tmB;
+        const uint8_t* sfa0 = p.sfa;
+        const uint8_t* sfb0 = p.sfb;
+        const float* sga0 = p.sga;
+        const float* sgb0 = p.sgb;
+        int64_t sgb_ld = p.sgb_ld;
+        if constexpr (GROUPED) {
+          const GroupDesc& G = gt->g[U.g];
+          mA = &G.tmA;
+          mB = &G.tmB;
+          sfa0 = G.sfa;
+          sfb0 = G.sfb;
+          sga0 = G.sga;
+          sgb0 = G.sgb;
+          sgb_ld = G.sgb_ld;
+        }
+        const uint8_t* sa = sfa0 + (int64_t)U.mb * p.sfa_kg * ATOM;
+        const uint8_t* sb = sfb0 + (int64_t)rb0 * p.sfb_kg * ATOM;
+        const float* ga = sga0 + (p.sga_ld ? m0 : 0);
+        const float* gb = sgb0 + (sgb_ld ? n0 : 0);
         int sb_bytes = BN * 4;
-        if (p.sgb_ld && p.sgb_ld - n0 < BN) sb_bytes = (int)(p.sgb_ld - n0) * 4;
+        if (sgb_ld && sgb_ld - n0 < BN) sb_bytes = (int)(sgb_ld - n0) * 4;
         int chunk = U.c_lo;
         for (int s = U.s_lo; s < U.s_hi; ++s) {
           const uint32_t fb = a_full + st * 8;
           mbar_wait_a(a_empty + st * 8, ph ^ 1);
           expect_tx_e(fb, tx);
-          tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, &tmA, fb, s * (KSTAGE / 2), m0);
+          tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, mA, fb, s * (KSTAGE / 2), m0);
           if constexpr (CL == 1) {
-            tma_load_2d_e(a_smem + OFF_B + st * STAGE_B, &tmB, fb, s * (KSTAGE / 2), n0);
+            tma_load_2d_e(a_smem + OFF_B + st * STAGE_B, mB, fb, s * (KSTAGE / 2), n0);
           } else {
-            tma_load_2d_mc_e(a_smem + OFF_B + st * STAGE_B + crank * (BN / CL) * (KSTAGE / 2), &tmB, fb,
+            tma_load_2d_mc_e(a_smem + OFF_B + st * STAGE_B + crank * (BN / CL) * (KSTAGE / 2), mB, fb,
                              s * (KSTAGE / 2), n0 + (int)crank * (BN / CL), (uint16_t)((1u << CL) - 1));
           }
           bulk_load_e(a_smem + OFF_SFA + st * SFA_BYTES, sa + (int64_t)s * SFA_BYTES, SFA_BYTES, fb);
@@ -373,7 +420,7 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
             expect_tx_e(sfb, BM * 4 + sb_bytes);
             const uint32_t dst = a_smem + OFF_SIG + slot * SIG_SLOT;
             bulk_load_e(dst, ga + (int64_t)chunk * p.sga_ld, BM * 4, sfb);
-            bulk_load_e(dst + BM * 4, gb + (int64_t)chunk * p.sgb_ld, sb_bytes, sfb);
+            bulk_load_e(dst + BM * 4, gb + (int64_t)chunk * sgb_ld, sb_bytes, sfb);
             if (++slot == NSIG) { slot = 0; sph ^= 1; }
             ++chunk;
           }
@@ -490,40 +537,42 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
         if (++slot == NSIG) { slot = 0; sph ^= 1; }
       }
       // store the tile row (masked to M x N): the output, or this split's f32 partial
+      void* const cout = GROUPED ? gt->g[U.g].c : p.c;
+      const int n_out = GROUPED ? gt->g[U.g].n : p.N;
       if (TRANS && row < p.M) {
         // kernel row = weight row n, kernel column = token: C[token][n] (and the
         // split partials in the same output orientation)
         if (ksplit > 1) {
-          float* out = p.ws + ((int64_t)U.split * p.N + col0) * p.ws_ld + row;
+          float* out = p.ws + ((int64_t)U.split * n_out + col0) * p.ws_ld + row;
 #pragma unroll
           for (int i = 0; i < COLS; ++i)
-            if (col0 + i < p.N) out[(int64_t)i * p.ws_ld] = acc[i];
+            if (col0 + i < n_out) out[(int64_t)i * p.ws_ld] = acc[i];
         } else if constexpr (OUT_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)col0 * p.ldc + row;
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(cout) + (int64_t)col0 * p.ldc + row;
 #pragma unroll
           for (int i = 0; i < COLS; ++i)
-            if (col0 + i < p.N) out[(int64_t)i * p.ldc] = __float2bfloat16_rn(acc[i]);
+            if (col0 + i < n_out) out[(int64_t)i * p.ldc] = __float2bfloat16_rn(acc[i]);
         } else {
-          float* out = reinterpret_cast<float*>(p.c) + (int64_t)col0 * p.ldc + row;
+          float* out = reinterpret_cast<float*>(cout) + (int64_t)col0 * p.ldc + row;
 #pragma unroll
           for (int i = 0; i < COLS; ++i)
-            if (col0 + i < p.N) out[(int64_t)i * p.ldc] = acc[i];
+            if (col0 + i < n_out) out[(int64_t)i * p.ldc] = acc[i];
         }
       } else if (row < p.M) {
         if (ksplit > 1) {
           float* out = p.ws + ((int64_t)U.split * p.M + row) * p.ws_ld + col0;
-          if (col0 + COLS <= p.N) {
+          if (col0 + COLS <= n_out) {
 #pragma unroll
             for (int i = 0; i < COLS; i += 4)
               *reinterpret_cast<float4*>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
           } else {
 #pragma unroll
             for (int i = 0; i < COLS; ++i)
-              if (col0 + i < p.N) out[i] = acc[i];
+              if (col0 + i < n_out) out[i] = acc[i];
           }
         } else if constexpr (OUT_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
-          if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
+          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(cout) + (int64_t)row * p.ldc + col0;
+          if (col0 + COLS <= n_out && (p.ldc % 8) == 0) {
 #pragma unroll
             for (int i = 0; i < COLS; i += 8) {
               uint4 w;
@@ -536,18 +585,18 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
           } else {
 #pragma unroll
             for (int i = 0; i < COLS; ++i)
-              if (col0 + i < p.N) out[i] = __float2bfloat16_rn(acc[i]);
+              if (col0 + i < n_out) out[i] = __float2bfloat16_rn(acc[i]);
           }
         } else {
-          float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + col0;
-          if (col0 + COLS <= p.N && (p.ldc % 4) == 0) {
+          float* out = reinterpret_cast<float*>(cout) + (int64_t)row * p.ldc + col0;
+          if (col0 + COLS <= n_out && (p.ldc % 4) == 0) {
 #pragma unroll
             for (int i = 0; i < COLS; i += 4)
               *reinterpret_cast<float4*>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
           } else {
 #pragma unroll
             for (int i = 0; i < COLS; ++i)
-              if (col0 + i < p.N) out[i] = acc[i];
+              if (col0 + i < n_out) out[i] = acc[i];
           }
         }
       }
@@ -561,6 +610,19 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
+}
+
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
+__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
+    k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ Params p) {
+  mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, TRANS, FUSED, false>(&tmA, &tmB, p, nullptr);
+}
+
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL>
+__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
+    k_gemm_mbs_grouped(const __grid_constant__ GroupTable gt) {
+  mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, true, false, true>(nullptr, nullptr, gt.p, &gt);
 }
 
 // Split-K partials: C = sum over splits (ascending) of ws[split], as bf16 or f32.
@@ -656,6 +718,76 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   return check_launch();
 }
 
+// Grouped swap-AB launch: kernel A = weights w[g] (one shared shape), kernel
+// B = tokens x[g] (<= BN rows each), C[g] = x[g] . w[g]^T stored [token][n].
+template <int BN, bool OUT_BF16, int CL>
+static int launch_grouped(const QDesc* w, const QDesc* x, void* const* c, int n, int64_t ldc, cudaStream_t st) {
+  using C = MbsCfg<BN, 4, 4>;
+  constexpr int SMEM = C::SMEM;
+  auto kern = k_gemm_mbs_grouped<BN, 4, 4, OUT_BF16, CL>;
+  static std::atomic<uint64_t> attr_set{0};
+  if (const int rc0 = smem_attr_once(kern, SMEM, attr_set)) return rc0;
+  const float* ones = ones_buffer();
+  if (!ones) return set_error(ERR_INVALID, "could not allocate the sigma ones row");
+  const QDesc& a = w[0];
+  const QDesc& b = x[0];
+  const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
+  std::unique_ptr<GroupTable> t(new GroupTable());
+  for (int g0 = 0; g0 < n; g0 += MAXG) {
+    const int ng = std::min(MAXG, n - g0);
+    memset(t.get(), 0, sizeof(GroupTable));
+    Params& p = t->p;
+    p.sfa_kg = a.sf_kpad / 4;
+    p.sfb_kg = b.sf_kpad / 4;
+    p.sfb_rb = (int)((b.rows + 255) / 256 * 2);
+    p.sga_ld = ma ? a.sig_t_ld : 0;
+    p.ldc = ldc;
+    p.M = (int)a.rows;
+    p.N = BN;
+    p.K = (int)a.cols;
+    const int macro = ma ? a.macro_size : b.macro_size;
+    p.mac_steps = macro / KSTEP;
+    p.n_chunks = (int)((a.cols + macro - 1) / macro);
+    p.ksplit = 1;
+    p.trace = nullptr;
+    p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+    t->n_groups = ng;
+    for (int j = 0; j < ng; ++j) {
+      const QDesc& wg = w[g0 + j];
+      const QDesc& xg = x[g0 + j];
+      GroupDesc& G = t->g[j];
+      int rc = make_code_map(&G.tmA, wg.codes, wg.rows, wg.cols / 2, wg.codes_ld, BM);
+      if (rc) return rc;
+      rc = make_code_map(&G.tmB, xg.codes, xg.rows, xg.cols / 2, xg.codes_ld, BN / CL);
+      if (rc) return rc;
+      G.sfa = wg.scales_mma;
+      G.sfb = xg.scales_mma;
+      G.sga = ma ? wg.sig_t : ones;
+      G.sgb = mbb ? xg.sig_t : ones;
+      G.sgb_ld = mbb ? xg.sig_t_ld : 0;
+      G.c = c[g0 + j];
+      G.n = (int)xg.rows;
+    }
+    const int units = ng * (((p.M + BM - 1) / BM + CL - 1) / CL);
+    const int clusters = std::min(units, num_sms() / CL);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * CL);
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, *t);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
+  return check_launch();
+}
+
 }  // namespace mbs
 
 // MBS pair on the tcgen05 path: macro sizes 64, 128, 256 (chunks never
@@ -723,6 +855,36 @@ int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_
     return launch_shape<64, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
   }
   return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
+}
+
+// Grouped decode GEMMs (a[g]: tokens, b[g]: weights of one shared shape).
+// ERR_UNSUPPORTED when the groups do not fit the grouped kernel (the caller
+// then runs them one by one).
+int launch_gemm_mbs_grouped(const QDesc* a, const QDesc* b, int n, void* const* c, int c_dtype, int64_t ldc,
+                            cudaStream_t st) {
+  if (n < 1) return set_error(ERR_INVALID, "no groups");
+  int max_tok = 0;
+  for (int g = 0; g < n; ++g) {
+    const QDesc& x = a[g];
+    const QDesc& w = b[g];
+    if (!gemm_mbs_supported(x, w) || x.rows < 1 || x.rows > 64 || w.rows < 256 || x.cols != w.cols ||
+        w.rows != b[0].rows || w.cols != b[0].cols || w.variant != b[0].variant || x.variant != a[0].variant ||
+        w.macro_size != b[0].macro_size || x.macro_size != a[0].macro_size || w.sf_kpad != b[0].sf_kpad ||
+        x.sf_kpad != a[0].sf_kpad || w.sig_t_ld != b[0].sig_t_ld || (x.rows + 255) / 256 != 1)
+      return set_error(ERR_UNSUPPORTED, "groups do not share one grouped-kernel shape");
+    max_tok = std::max(max_tok, (int)x.rows);
+  }
+  const bool bf = c_dtype == MXQ_BF16;
+  const bool cl2 = (b[0].rows + mbs::BM - 1) / mbs::BM >= 2;
+#define MXQ_GRP(BN_)                                                                                    \
+  return cl2 ? (bf ? mbs::launch_grouped<BN_, true, 2>(b, a, c, n, ldc, st)                            \
+                   : mbs::launch_grouped<BN_, false, 2>(b, a, c, n, ldc, st))                          \
+             : (bf ? mbs::launch_grouped<BN_, true, 1>(b, a, c, n, ldc, st)                            \
+                   : mbs::launch_grouped<BN_, false, 1>(b, a, c, n, ldc, st))
+  if (max_tok <= 16) MXQ_GRP(16);
+  if (max_tok <= 32) MXQ_GRP(32);
+  MXQ_GRP(64);
+#undef MXQ_GRP
 }
 
 bool gemm_mbs_fusable(const QDesc& a, const QDesc& b, int x_dtype) {

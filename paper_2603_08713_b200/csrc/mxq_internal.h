@@ -48,6 +48,8 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
 bool gemm_mbs_supported(const QDesc& a, const QDesc& b);
 int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t ldc, cudaStream_t st);
 bool gemm_mbs_fusable(const QDesc& a, const QDesc& b, int x_dtype);
+int launch_gemm_mbs_grouped(const QDesc* a, const QDesc* b, int n, void* const* c, int c_dtype, int64_t ldc,
+                            cudaStream_t st);
 int launch_gemm_mbs_fused(const void* x, int64_t x_ld, const QDesc& a, const QDesc& b, void* c, int c_dtype,
                           int64_t ldc, uint32_t* status, cudaStream_t st);
 void set_gemm_trace(long long* p);

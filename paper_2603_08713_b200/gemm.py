@@ -21,7 +21,8 @@ import torch
 from . import _lib
 from .quantize import QuantizedTensor, SchemeConfig, Variant, quantize_tensor
 
-__all__ = ["TileConfig", "OverheadReport", "matmul_reference", "matmul_quantized", "quantize_matmul",
+__all__ = ["TileConfig", "OverheadReport", "matmul_reference", "matmul_quantized", "matmul_quantized_grouped",
+           "quantize_matmul",
            "roofline_overhead", "max_ulp_divergence", "tc_supported"]
 
 
@@ -128,6 +129,44 @@ def matmul_quantized(aq: QuantizedTensor, bq: QuantizedTensor, cfg: TileConfig =
     _lib.check(L.mxq_gemm(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), dt, c.stride(0), status.data_ptr(),
                           stream), "matmul_quantized")
     return c
+
+
+def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dtype: torch.dtype = torch.float32,
+                             check: bool = True) -> list:
+    """``[matmul_quantized(a, b) for a, b in zip(aqs, bqs)]`` for MoE-style
+    expert GEMMs (SURVEY section 8 d config 5): ``aqs[g]`` the tokens routed
+    to expert g (at most 64 rows for the grouped kernel), ``bqs[g]`` that
+    expert's weights, all of one shape.  MBS / E8M0 pairs of one variant pair
+    run as one launch of the swap-AB MBS kernel per 64 experts
+    (csrc/gemm_mbs.cu ``k_gemm_mbs_grouped``); other pairs fall back to one
+    launch per expert.  Tolerance parity as ``matmul_quantized``."""
+    aqs, bqs = list(aqs), list(bqs)
+    if len(aqs) != len(bqs) or not aqs:
+        raise ValueError("need one weight per token group")
+    n = bqs[0].shape[0]
+    for aq, bq in zip(aqs, bqs):
+        if aq.shape[1] != bq.shape[1]:
+            raise ValueError(f"operands disagree on K: {aq.shape} vs {bq.shape}")
+        if bq.shape != bqs[0].shape:
+            raise ValueError("every expert's weights must have one shape")
+        _validate_chunking(aq, cfg.t_k, "a")
+        _validate_chunking(bq, cfg.t_k, "b")
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("out_dtype must be float32 or bfloat16")
+    if not all(tc_supported(aq, bq) for aq, bq in zip(aqs, bqs)) or any(
+            aq.variant is Variant.NVFP4 for aq in aqs):
+        return [matmul_quantized(aq, bq, cfg, out_dtype=out_dtype, check=check) for aq, bq in zip(aqs, bqs)]
+    dev = aqs[0].codes.device
+    outs = [torch.empty((aq.shape[0], n), dtype=out_dtype, device=dev) for aq in aqs]
+    sfb = 16  # (an MBS operand makes every pair block-16)
+    qa = (_lib.QT * len(aqs))(*[aq.gemm_qt(sfb) for aq in aqs])
+    qb = (_lib.QT * len(bqs))(*[bq.gemm_qt(sfb) for bq in bqs])
+    cp = (ctypes.c_void_p * len(outs))(*[o.data_ptr() for o in outs])
+    status = torch.zeros(4, dtype=torch.int32, device=dev)
+    dt = _lib.MXQ_BF16 if out_dtype == torch.bfloat16 else _lib.MXQ_F32
+    _lib.check(_lib.lib().mxq_gemm_grouped(qa, qb, len(aqs), ctypes.cast(cp, ctypes.c_void_p), dt, n,
+                                           status.data_ptr(), _lib.stream_handle()), "matmul_quantized_grouped")
+    return outs
 
 
 def quantize_matmul(a, bq: QuantizedTensor, cfg: SchemeConfig = SchemeConfig(Variant.MBS_S),

@@ -208,3 +208,36 @@ def test_quantize_matmul_fused_repeated_and_nonfinite():
     bad[300, 7] = float("nan")
     with pytest.raises(ValueError):
         M.quantize_matmul(bad, wq)
+
+
+# ---------------------------------------------------------------------------
+# Grouped expert GEMMs (config 5): one launch per 64 experts of the swap-AB
+# MBS kernel, each group against the dequantize-then-f64 reference.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("toks,n,k,wv,av,out_dtype", [
+    ([1, 5, 16, 3], 640, 2880, "mbs_d", "mbs_s", torch.float32),      # K = 2880: short last macro and stage
+    ([33, 64, 17], 384, 1024, "mbs_d", "mbs_s", torch.bfloat16),
+    ([8] * 70, 256, 512, "mbs_d", "mbs_s", torch.float32),            # 70 groups: two launches
+    ([2, 9], 512, 1024, "mx16_oas", "mbs_s", torch.float32),          # non-MBS weights
+    ([4, 4], 512, 1024, "nvfp4", "nvfp4", torch.float32),             # per-group fallback
+])
+def test_grouped_expert_gemm_matches_reference(toks, n, k, wv, av, out_dtype):
+    g = torch.Generator(device="cuda").manual_seed(11 + len(toks) + n)
+    aqs, bqs = [], []
+    for t in toks:
+        a = torch.distributions.StudentT(4.0).sample((t, k)).to("cuda") if t % 2 else torch.randn(t, k, device="cuda", generator=g)
+        w = torch.randn(n, k, device="cuda", generator=g) * 0.02
+        aqs.append(M.quantize_tensor(a.to(torch.bfloat16), M.SchemeConfig(M.Variant(av))))
+        bqs.append(M.quantize_tensor(w.to(torch.bfloat16), M.SchemeConfig(M.Variant(wv))))
+    cs = M.matmul_quantized_grouped(aqs, bqs, out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    for i, (aq, bq, c) in enumerate(zip(aqs, bqs, cs)):
+        da, db = M.dequantize_tensor(aq).double(), M.dequantize_tensor(bq).double()
+        want, bound = (da @ db.T).cpu().numpy(), (da.abs() @ db.abs().T).cpu().numpy()
+        got = c.float().cpu().numpy()
+        if out_dtype == torch.float32:
+            _check(got, want, bound, ("grouped", i, toks[i]))
+        else:
+            single = M.matmul_quantized(aq, bq, out_dtype=torch.float32).cpu().numpy()
+            _check(single, want, bound, ("single", i))
+            assert np.allclose(got, single, rtol=2 ** -7, atol=1e-6 * np.abs(single).max()), i
