@@ -140,19 +140,29 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   const double st = (has_q && q.variant == NVFP4 && q.tensor_scale) ? *q.tensor_scale : 1.0;
   uint32_t bad = 0;
   unsigned long long nz = 0, fl = 0;
+  // element -> (row, col) without a 64-bit division per element: one per
+  // leaf (warp-uniform), then a 32-bit carry (or division for rows shorter
+  // than a leaf); block / macro indices by shift or 32-bit division
+  const uint32_t ucols = (uint32_t)cols;
+  const int bs_shift = has_q ? (q.block_size == 32 ? 5 : 4) : 4;
+  const uint32_t umacro = has_q && q.mant ? (uint32_t)q.macro_size : 1u;
   for (int li = warp; li < nl; li += QS_WARPS) {
     const Range lf = s_leaf[li];
+    const int64_t row0 = lf.s / cols;
+    const uint32_t c0 = (uint32_t)(lf.s - row0 * cols);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int64_t p = 4 * lane + j;
       double a = 0.0, b = 0.0;
       if (p < lf.n) {
-        const int64_t e = lf.s + p;
-        const int64_t r = e / cols, c = e - r * cols;
+        const uint32_t cc = c0 + (uint32_t)p;
+        const uint32_t dr = ucols >= 128u ? (cc >= ucols ? 1u : 0u) : cc / ucols;
+        const int64_t r = row0 + dr;
+        const uint32_t c = cc - dr * ucols;
         const float rv = load_ref(ref, dtype, r * ref_ld + c);
         float xv;
         uint32_t code = 1;
-        if (has_q) xv = q_elem(q, st, r, c, code, bad);
+        if (has_q) xv = q_elem_fast(q, st, r, c, bs_shift, umacro, code, bad);
         else xv = recon[r * recon_ld + c];
         const double r64 = (double)rv;
         const double d = __dsub_rn(r64, (double)xv);
@@ -196,8 +206,30 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
     if (bad) atomicOr(status, bad);
   }
   __syncthreads();
+  // A node of 128 * 2^k elements (every node but the tail ones of an
+  // irregular n) is a perfect tree of equal 128-element leaves: fold it level
+  // by level with all threads (adjacent pairs, index order -- the same
+  // additions as the serial fold).  Otherwise thread 0 walks numpy's split
+  // recursion.
+  const bool perfect = nl > 0 && nl <= 2 * QS_THREADS && (nl & (nl - 1)) == 0 && node.n == 128LL * nl;
+  if (perfect) {
+    for (int width = nl; width > 1; width >>= 1) {
+      const int half = width >> 1, i = threadIdx.x;
+      double va = 0.0, vb = 0.0;
+      if (i < half) {
+        va = __dadd_rn(s_la[2 * i], s_la[2 * i + 1]);
+        vb = __dadd_rn(s_lb[2 * i], s_lb[2 * i + 1]);
+      }
+      __syncthreads();
+      if (i < half) {
+        s_la[i] = va;
+        s_lb[i] = vb;
+      }
+      __syncthreads();
+    }
+  }
   if (threadIdx.x == 0) {
-    PairSum ps = fold_node(node.n, s_la, s_lb, s_frames);
+    const PairSum ps = perfect ? PairSum{s_la[0], s_lb[0]} : fold_node(node.n, s_la, s_lb, s_frames);
     const int64_t nodes = (int64_t)1 << depth;
     ws[blockIdx.x] = ps.a;
     ws[nodes + blockIdx.x] = ps.b;
@@ -210,20 +242,27 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
 // Fold of the top `depth` levels.  Every CTA node sits at depth d of a
 // perfect binary tree (a numpy leaf above depth d continues as "left = itself,
 // right = empty (0.0)"), so the top of the tree is a plain pairwise
-// reduction of the 2^d node sums in index order -- done in place.
-__global__ void k_qsnr_top(int64_t n, int depth, double* __restrict__ ws, double* __restrict__ out4) {
+// reduction of the 2^d node sums in index order: one CTA, level by level,
+// ping-ponging between the node sums and a second buffer in the workspace.
+constexpr int QS_TOP_THREADS = 1024;
+__global__ void __launch_bounds__(QS_TOP_THREADS) k_qsnr_top(int64_t n, int depth, double* __restrict__ ws,
+                                                            double* __restrict__ out4) {
   const int64_t nodes = (int64_t)1 << depth;
   double* sa = ws;
   double* sb = ws + nodes;
+  double* ta = ws + 2 * nodes + 2;
+  double* tb = ta + nodes;
   for (int64_t width = nodes; width > 1; width >>= 1) {
-    // single thread, ascending i: slot i is written only after slots 2i and
-    // 2i+1 (>= i) have been read
-    for (int64_t i = 0; i < width / 2; ++i) {
-      sa[i] = __dadd_rn(sa[2 * i], sa[2 * i + 1]);
-      sb[i] = __dadd_rn(sb[2 * i], sb[2 * i + 1]);
+    const int64_t half = width >> 1;
+    for (int64_t i = threadIdx.x; i < half; i += QS_TOP_THREADS) {
+      ta[i] = __dadd_rn(sa[2 * i], sa[2 * i + 1]);
+      tb[i] = __dadd_rn(sb[2 * i], sb[2 * i + 1]);
     }
+    __syncthreads();
+    double* t = sa; sa = ta; ta = t;
+    t = sb; sb = tb; tb = t;
   }
-  {
+  if (threadIdx.x == 0) {
     const unsigned long long* cnt = reinterpret_cast<const unsigned long long*>(ws + 2 * nodes);
     out4[0] = sa[0];
     out4[1] = sb[0];
@@ -235,7 +274,7 @@ __global__ void k_qsnr_top(int64_t n, int depth, double* __restrict__ ws, double
 
 int64_t qsnr_workspace_bytes(int64_t n) {
   const int d = qs_depth(n);
-  return (int64_t)sizeof(double) * (2 * ((int64_t)1 << d) + 2);
+  return (int64_t)sizeof(double) * (4 * ((int64_t)1 << d) + 2);  // node sums, counts, top-fold ping-pong
 }
 
 int launch_qsnr(const void* ref, int dtype, int64_t ref_ld, const QDesc* q, const float* recon, int64_t recon_ld,
@@ -250,7 +289,7 @@ int launch_qsnr(const void* ref, int dtype, int64_t ref_ld, const QDesc* q, cons
   if (q) qd = *q;
   k_qsnr_nodes<<<(unsigned)nodes, QS_THREADS, 0, st>>>(ref, dtype, ref_ld, qd, q ? 1 : 0, recon, recon_ld, rows,
                                                          cols, d, w, status);
-  k_qsnr_top<<<1, 1, 0, st>>>(n, d, w, out4);
+  k_qsnr_top<<<1, QS_TOP_THREADS, 0, st>>>(n, d, w, out4);
   return check_launch();
 }
 
