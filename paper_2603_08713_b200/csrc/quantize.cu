@@ -503,29 +503,50 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
 // K5: dequantise to f32 (src/quantize.py:728-746).  Thread == block.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_dequantize(QDesc q, float* __restrict__ out, int64_t out_ld,
-                                                    uint32_t* __restrict__ status) {
+                                                    FastDiv fd_nbr, uint32_t nb, uint32_t* __restrict__ status) {
   const int bs = q.block_size;
-  const int64_t nbr = q.cols / bs, nb = q.rows * nbr;
+  const uint32_t nbr = fd_nbr.d;
   const double st = (q.variant == NVFP4 && q.tensor_scale) ? *q.tensor_scale : 1.0;
   uint32_t bad = 0;
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = b / nbr, kb = b - r * nbr;
-    const uint32_t s = q.scales[r * q.scales_ld + kb];
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const uint32_t r = fdiv(b, fd_nbr), kb = b - r * nbr;
+    const uint32_t s = q.scales[(int64_t)r * q.scales_ld + kb];
     uint32_t m8 = 0;
-    if (q.mant) m8 = q.mant[r * q.mant_ld + (kb * bs) / q.macro_size];
+    if (q.mant) m8 = q.mant[(int64_t)r * q.mant_ld + (kb * bs) / q.macro_size];
     if (q.variant == NVFP4) bad |= ((s & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
     else bad |= (s == 255u) ? ST_BAD_E8M0 : 0u;
-    const uint8_t* cp = q.codes + r * q.codes_ld + kb * (bs / 2);
-    float* op = out + r * out_ld + kb * bs;
+    // Fast path (E8M0 variants, 4 <= biased <= 250, every value f32-normal):
+    // the grid is {0.5, 1, 2, 4} x 1 and {1, 2, 4} x 1.5, so with
+    // u = RN(1/f), v = RN(1.5/f) (f = 1+m8/256, or 1) every magnitude is
+    // u or v times 2^((idx>>1) - 1 + biased - 127) -- an exact power-of-two
+    // scaling of the same correctly rounded quotient deq_mbs computes.
+    const bool fast = q.variant != NVFP4 && s >= 4u && s <= 250u;
+    float u = 1.0f, v = 1.5f;
+    if (fast && q.mant) {
+      const float f = mbs_factor(m8);
+      u = __fdiv_rn(1.0f, f);
+      v = __fdiv_rn(1.5f, f);
+    }
+    const uint8_t* cp = q.codes + (int64_t)r * q.codes_ld + kb * (bs / 2);
+    float* op = out + (int64_t)r * out_ld + (int64_t)kb * bs;
     for (int w = 0; w < bs / 8; ++w) {
       const uint32_t word = *reinterpret_cast<const uint32_t*>(cp + 4 * w);
       float o[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t c = (word >> (4 * j)) & 15u;
-        if (q.variant == NVFP4) o[j] = deq_nvfp4(c, s, st);
-        else if (q.mant) o[j] = deq_mbs(c, s, m8);
-        else o[j] = deq_pow2(c, s);
+        if (fast) {
+          const uint32_t idx = c & 7u;
+          const float base = ((idx & 1u) && idx > 1u) ? v : u;
+          const float mag = idx ? base * __uint_as_float((uint32_t)((int)(idx >> 1) - 1 + (int)s) << 23) : 0.0f;
+          o[j] = (c & 8u) ? -mag : mag;
+        } else if (q.variant == NVFP4) {
+          o[j] = deq_nvfp4(c, s, st);
+        } else if (q.mant) {
+          o[j] = deq_mbs(c, s, m8);
+        } else {
+          o[j] = deq_pow2(c, s);
+        }
       }
       float4* o4 = reinterpret_cast<float4*>(op + 8 * w);
       __stcs(o4, make_float4(o[0], o[1], o[2], o[3]));
@@ -658,7 +679,9 @@ int launch_quantize_lut(const void* x, int dtype, int64_t x_ld, const QDesc& q, 
 
 int launch_dequantize(const QDesc& q, float* out, int64_t out_ld, uint32_t* status, cudaStream_t st) {
   const int64_t nb = q.rows * (q.cols / q.block_size);
-  k_dequantize<<<grid_for(nb, 256), 256, 0, st>>>(q, out, out_ld, status);
+  if (nb >= ((int64_t)1 << 31)) return set_error(ERR_UNSUPPORTED, "tensor too large (>= 2^31 blocks)");
+  k_dequantize<<<grid_for(nb, 256), 256, 0, st>>>(q, out, out_ld, make_fastdiv((uint32_t)(q.cols / q.block_size)),
+                                                  (uint32_t)nb, status);
   return check_launch();
 }
 
