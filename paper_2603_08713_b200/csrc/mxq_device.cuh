@@ -23,20 +23,4 @@ __device__ __forceinline__ float q_elem(const QDesc& q, double st, int64_t r, in
   return deq_pow2(code, s);
 }
 
-// q_elem with 32-bit column math: block index by shift (block size 16 / 32),
-// macro index by a 32-bit division (macro sizes are any multiple of 16).
-__device__ __forceinline__ float q_elem_fast(const QDesc& q, double st, int64_t r, uint32_t c, int bs_shift,
-                                             uint32_t macro, uint32_t& code, uint32_t& bad) {
-  const uint8_t byte = q.codes[r * q.codes_ld + (c >> 1)];
-  code = (c & 1) ? (byte >> 4) : (byte & 15u);
-  const uint32_t s = q.scales[r * q.scales_ld + (c >> bs_shift)];
-  if (q.variant == NVFP4) {
-    bad |= ((s & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
-    return deq_nvfp4(code, s, st);
-  }
-  bad |= (s == 255u) ? ST_BAD_E8M0 : 0u;
-  if (q.mant) return deq_mbs(code, s, q.mant[r * q.mant_ld + c / macro]);
-  return deq_pow2(code, s);
-}
-
 }  // namespace mxq

@@ -150,31 +150,77 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
     const Range lf = s_leaf[li];
     const int64_t row0 = lf.s / cols;
     const uint32_t c0 = (uint32_t)(lf.s - row0 * cols);
+    // A lane's 4 elements (p0..p0+3) lie in one row and one 16-block: leaves
+    // start at multiples of 8 and rows are multiples of 16 long.  Row, block,
+    // scale, mantissa and the two dequantisation quotients are computed once
+    // per lane per leaf (the first version spent ~220 instructions per element
+    // on per-element index math and divisions).
+    const int p0 = 4 * lane;
+    double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (p0 < lf.n) {
+      const uint32_t cc = c0 + (uint32_t)p0;
+      const uint32_t dr = ucols >= 128u ? (cc >= ucols ? 1u : 0u) : cc / ucols;
+      const int64_t r = row0 + dr;
+      const uint32_t c = cc - dr * ucols;
+      float xv[4];
+      uint32_t codes4 = 0x1111u;  // (dense recon: no flush statistics)
+      if (has_q) {
+        const uint8_t* cp = q.codes + r * q.codes_ld + (c >> 1);
+        codes4 = (uint32_t)cp[0] | ((uint32_t)cp[1] << 8);
+        const uint32_t sc = q.scales[r * q.scales_ld + (c >> bs_shift)];
+        if (q.variant == NVFP4) {
+          bad |= ((sc & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t p = 4 * lane + j;
-      double a = 0.0, b = 0.0;
-      if (p < lf.n) {
-        const uint32_t cc = c0 + (uint32_t)p;
-        const uint32_t dr = ucols >= 128u ? (cc >= ucols ? 1u : 0u) : cc / ucols;
-        const int64_t r = row0 + dr;
-        const uint32_t c = cc - dr * ucols;
-        const float rv = load_ref(ref, dtype, r * ref_ld + c);
-        float xv;
-        uint32_t code = 1;
-        if (has_q) xv = q_elem_fast(q, st, r, c, bs_shift, umacro, code, bad);
-        else xv = recon[r * recon_ld + c];
+          for (int j = 0; j < 4; ++j) xv[j] = deq_nvfp4((codes4 >> (4 * j)) & 15u, sc, st);
+        } else {
+          bad |= (sc == 255u) ? ST_BAD_E8M0 : 0u;
+          const uint32_t m8 = q.mant ? q.mant[r * q.mant_ld + c / umacro] : 0u;
+          if (sc >= 4u && sc <= 250u) {
+            // exact: every magnitude is RN(1/f) or RN(1.5/f) times a power of
+            // two (see k_dequantize)
+            float u = 1.0f, v = 1.5f;
+            if (q.mant) {
+              const float f = mbs_factor(m8);
+              u = __fdiv_rn(1.0f, f);
+              v = __fdiv_rn(1.5f, f);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t code = (codes4 >> (4 * j)) & 15u, idx = code & 7u;
+              const float base = ((idx & 1u) && idx > 1u) ? v : u;
+              const float mag =
+                  idx ? base * __uint_as_float((uint32_t)((int)(idx >> 1) - 1 + (int)sc) << 23) : 0.0f;
+              xv[j] = (code & 8u) ? -mag : mag;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t code = (codes4 >> (4 * j)) & 15u;
+              xv[j] = q.mant ? deq_mbs(code, sc, m8) : deq_pow2(code, sc);
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xv[j] = recon[r * recon_ld + c + j];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float rv = load_ref(ref, dtype, r * ref_ld + c + j);
         const double r64 = (double)rv;
-        const double d = __dsub_rn(r64, (double)xv);
-        a = __dmul_rn(r64, r64);
-        b = __dmul_rn(d, d);
+        const double d = __dsub_rn(r64, (double)xv[j]);
+        a4[j] = __dmul_rn(r64, r64);
+        b4[j] = __dmul_rn(d, d);
         if (rv != 0.0f) {
           ++nz;
-          if ((code & 7u) == 0) ++fl;
+          if (((codes4 >> (4 * j)) & 7u) == 0) ++fl;
         }
       }
-      s_sq[warp][0][p] = a;
-      s_sq[warp][1][p] = b;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      s_sq[warp][0][p0 + j] = a4[j];
+      s_sq[warp][1][p0 + j] = b4[j];
     }
     __syncwarp();
     // lanes 0-7: signal accumulators r[j]; lanes 8-15: error accumulators.
@@ -183,7 +229,8 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
       const double* v = s_sq[warp][lane >> 3];
       const int j = lane & 7;
       acc = v[j];
-      for (int64_t i = 8; i < lf.n; i += 8) acc = __dadd_rn(acc, v[i + j]);
+      const int ln = (int)lf.n;
+      for (int i = 8; i < ln; i += 8) acc = __dadd_rn(acc, v[i + j]);
     }
     double r0 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 0), r1 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 1);
     double r2 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 2), r3 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 3);
