@@ -160,11 +160,12 @@ int mxq_gemm(const mxq_qtensor* a, const mxq_qtensor* b, void* c, int32_t c_dtyp
 /*
  * Grouped decode GEMMs (MoE experts; SURVEY section 8 d config 5): the n
  * independent products C_g = A_g . B_g^T (matmul_quantized src/gemm.py:137-172
- * per group), A_g the tokens routed to expert g (<= 64 rows), B_g the
+ * per group), A_g the tokens routed to expert g (<= 128 rows), B_g the
  * expert's weights, every B_g of one shape.  a, b: HOST arrays of n
  * descriptors; c: HOST array of n device output pointers (row stride ldc).
  * When the pairs are MBS / E8M0 pairs of one variant pair and macro size, all
- * groups run in one launch of the swap-AB MBS kernel per 64 groups; otherwise
+ * groups run in one launch of the MBS kernel per 64 groups (swap-AB up to
+ * 64 tokens, direct 128-row tiles up to 128); otherwise
  * one mxq_gemm launch per group.  Same tolerance parity as mxq_gemm.
  */
 int mxq_gemm_grouped(const mxq_qtensor* a, const mxq_qtensor* b, int32_t n, void* const* c, int32_t c_dtype,

@@ -136,7 +136,8 @@ struct GroupDesc {
   const float* sgb;
   int64_t sgb_ld;
   void* c;
-  int n;                 // tokens of this group (kernel N)
+  int n;                 // kernel N of this group (tokens, swap-AB form)
+  int m;                 // kernel M of this group (tokens, direct form)
 };
 struct GroupTable {
   Params p;
@@ -373,8 +374,6 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         const int rb0 = n0 / 128;
         const int nrb = (rb0 + NRB <= p.sfb_rb) ? NRB : p.sfb_rb - rb0;
         const uint32_t tx = STAGE_A + STAGE_B + SFA_BYTES + nrb * 4 * ATOM;
-        const CUtensorMap* mA = tmA;
-        const CUtensorMap* mB = tmB;
         const uint8_t* sfa0 = p.sfa;
         const uint8_t* sfb0 = p.sfb;
         const float* sga0 = p.sga;
@@ -382,8 +381,6 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         int64_t sgb_ld = p.sgb_ld;
         if constexpr (GROUPED) {
           const GroupDesc& G = gt->g[U.g];
-          mA = &G.tmA;
-          mB = &G.tmB;
           sfa0 = G.sfa;
           sfb0 = G.sfb;
           sga0 = G.sga;
@@ -399,6 +396,11 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         int chunk = U.c_lo;
         for (int s = U.s_lo; s < U.s_hi; ++s) {
           const uint32_t fb = a_full + st * 8;
+          // (grouped: the maps are re-derived per stage from the unit's group
+          // index -- param-space addresses -- to keep the producer loop within
+          // its 32 registers)
+          const CUtensorMap* mA = GROUPED ? &gt->g[U.g].tmA : tmA;
+          const CUtensorMap* mB = GROUPED ? &gt->g[U.g].tmB : tmB;
           mbar_wait_a(a_empty + st * 8, ph ^ 1);
           expect_tx_e(fb, tx);
           tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, mA, fb, s * (KSTAGE / 2), m0);
@@ -558,7 +560,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           for (int i = 0; i < COLS; ++i)
             if (col0 + i < n_out) out[(int64_t)i * p.ldc] = acc[i];
         }
-      } else if (row < p.M) {
+      } else if (row < (GROUPED ? gt->g[U.g].m : p.M)) {
         if (ksplit > 1) {
           float* out = p.ws + ((int64_t)U.split * p.M + row) * p.ws_ld + col0;
           if (col0 + COLS <= n_out) {
@@ -619,10 +621,10 @@ __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg
   mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, TRANS, FUSED, false>(&tmA, &tmB, p, nullptr);
 }
 
-template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL>
+template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS>
 __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
     k_gemm_mbs_grouped(const __grid_constant__ GroupTable gt) {
-  mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, true, false, true>(nullptr, nullptr, gt.p, &gt);
+  mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, TRANS, false, true>(nullptr, nullptr, gt.p, &gt);
 }
 
 // Split-K partials: C = sum over splits (ascending) of ws[split], as bf16 or f32.
@@ -718,19 +720,23 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   return check_launch();
 }
 
-// Grouped swap-AB launch: kernel A = weights w[g] (one shared shape), kernel
-// B = tokens x[g] (<= BN rows each), C[g] = x[g] . w[g]^T stored [token][n].
-template <int BN, bool OUT_BF16, int CL>
-static int launch_grouped(const QDesc* w, const QDesc* x, void* const* c, int n, int64_t ldc, cudaStream_t st) {
-  using C = MbsCfg<BN, 4, 4>;
+// Grouped launch.  TRANS (swap-AB, tokens <= 64): kernel A = the weights
+// ka[g] (one shared shape), kernel B = the tokens kb[g], C stored [token][n].
+// Direct form (tokens <= 128): kernel A = the tokens ka[g] (one 128-row
+// block), kernel B = the weights kb[g].  kernel_m / kernel_n: the shared
+// kernel extents (the per-group token counts mask the stores).
+template <int BN, int NB, int EPIW, bool OUT_BF16, int CL, bool TRANS>
+static int launch_grouped(const QDesc* ka, const QDesc* kb, void* const* c, int n, int64_t ldc, int kernel_m,
+                          int kernel_n, cudaStream_t st) {
+  using C = MbsCfg<BN, NB, EPIW>;
   constexpr int SMEM = C::SMEM;
-  auto kern = k_gemm_mbs_grouped<BN, 4, 4, OUT_BF16, CL>;
+  auto kern = k_gemm_mbs_grouped<BN, NB, EPIW, OUT_BF16, CL, TRANS>;
   static std::atomic<uint64_t> attr_set{0};
   if (const int rc0 = smem_attr_once(kern, SMEM, attr_set)) return rc0;
   const float* ones = ones_buffer();
   if (!ones) return set_error(ERR_INVALID, "could not allocate the sigma ones row");
-  const QDesc& a = w[0];
-  const QDesc& b = x[0];
+  const QDesc& a = ka[0];
+  const QDesc& b = kb[0];
   const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
   std::unique_ptr<GroupTable> t(new GroupTable());
   for (int g0 = 0; g0 < n; g0 += MAXG) {
@@ -742,8 +748,8 @@ static int launch_grouped(const QDesc* w, const QDesc* x, void* const* c, int n,
     p.sfb_rb = (int)((b.rows + 255) / 256 * 2);
     p.sga_ld = ma ? a.sig_t_ld : 0;
     p.ldc = ldc;
-    p.M = (int)a.rows;
-    p.N = BN;
+    p.M = kernel_m;
+    p.N = kernel_n;
     p.K = (int)a.cols;
     const int macro = ma ? a.macro_size : b.macro_size;
     p.mac_steps = macro / KSTEP;
@@ -753,22 +759,23 @@ static int launch_grouped(const QDesc* w, const QDesc* x, void* const* c, int n,
     p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
     t->n_groups = ng;
     for (int j = 0; j < ng; ++j) {
-      const QDesc& wg = w[g0 + j];
-      const QDesc& xg = x[g0 + j];
+      const QDesc& ag = ka[g0 + j];
+      const QDesc& bg = kb[g0 + j];
       GroupDesc& G = t->g[j];
-      int rc = make_code_map(&G.tmA, wg.codes, wg.rows, wg.cols / 2, wg.codes_ld, BM);
+      int rc = make_code_map(&G.tmA, ag.codes, ag.rows, ag.cols / 2, ag.codes_ld, BM);
       if (rc) return rc;
-      rc = make_code_map(&G.tmB, xg.codes, xg.rows, xg.cols / 2, xg.codes_ld, BN / CL);
+      rc = make_code_map(&G.tmB, bg.codes, bg.rows, bg.cols / 2, bg.codes_ld, BN / CL);
       if (rc) return rc;
-      G.sfa = wg.scales_mma;
-      G.sfb = xg.scales_mma;
-      G.sga = ma ? wg.sig_t : ones;
-      G.sgb = mbb ? xg.sig_t : ones;
-      G.sgb_ld = mbb ? xg.sig_t_ld : 0;
+      G.sfa = ag.scales_mma;
+      G.sfb = bg.scales_mma;
+      G.sga = ma ? ag.sig_t : ones;
+      G.sgb = mbb ? bg.sig_t : ones;
+      G.sgb_ld = mbb ? bg.sig_t_ld : 0;
       G.c = c[g0 + j];
-      G.n = (int)xg.rows;
+      G.n = TRANS ? (int)bg.rows : kernel_n;
+      G.m = TRANS ? kernel_m : (int)ag.rows;
     }
-    const int units = ng * (((p.M + BM - 1) / BM + CL - 1) / CL);
+    const int units = ng * (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
     const int clusters = std::min(units, num_sms() / CL);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(clusters * CL);
@@ -867,20 +874,26 @@ int launch_gemm_mbs_grouped(const QDesc* a, const QDesc* b, int n, void* const* 
   for (int g = 0; g < n; ++g) {
     const QDesc& x = a[g];
     const QDesc& w = b[g];
-    if (!gemm_mbs_supported(x, w) || x.rows < 1 || x.rows > 64 || w.rows < 256 || x.cols != w.cols ||
+    if (!gemm_mbs_supported(x, w) || x.rows < 1 || x.rows > 128 || w.rows < 256 || x.cols != w.cols ||
         w.rows != b[0].rows || w.cols != b[0].cols || w.variant != b[0].variant || x.variant != a[0].variant ||
         w.macro_size != b[0].macro_size || x.macro_size != a[0].macro_size || w.sf_kpad != b[0].sf_kpad ||
-        x.sf_kpad != a[0].sf_kpad || w.sig_t_ld != b[0].sig_t_ld || (x.rows + 255) / 256 != 1)
+        x.sf_kpad != a[0].sf_kpad || w.sig_t_ld != b[0].sig_t_ld || x.sig_t_ld != a[0].sig_t_ld ||
+        (x.rows + 255) / 256 != 1)
       return set_error(ERR_UNSUPPORTED, "groups do not share one grouped-kernel shape");
     max_tok = std::max(max_tok, (int)x.rows);
   }
   const bool bf = c_dtype == MXQ_BF16;
-  const bool cl2 = (b[0].rows + mbs::BM - 1) / mbs::BM >= 2;
-#define MXQ_GRP(BN_)                                                                                    \
-  return cl2 ? (bf ? mbs::launch_grouped<BN_, true, 2>(b, a, c, n, ldc, st)                            \
-                   : mbs::launch_grouped<BN_, false, 2>(b, a, c, n, ldc, st))                          \
-             : (bf ? mbs::launch_grouped<BN_, true, 1>(b, a, c, n, ldc, st)                            \
-                   : mbs::launch_grouped<BN_, false, 1>(b, a, c, n, ldc, st))
+  const int wrows = (int)b[0].rows;
+  if (max_tok > 64) {  // direct form: one 128-row token block per expert, 128 x 192 tiles over the weights
+    return bf ? mbs::launch_grouped<192, 2, 16, true, 1, false>(a, b, c, n, ldc, max_tok, wrows, st)
+              : mbs::launch_grouped<192, 2, 16, false, 1, false>(a, b, c, n, ldc, max_tok, wrows, st);
+  }
+  const bool cl2 = (wrows + mbs::BM - 1) / mbs::BM >= 2;
+#define MXQ_GRP(BN_)                                                                                              \
+  return cl2 ? (bf ? mbs::launch_grouped<BN_, 4, 4, true, 2, true>(b, a, c, n, ldc, wrows, BN_, st)              \
+                   : mbs::launch_grouped<BN_, 4, 4, false, 2, true>(b, a, c, n, ldc, wrows, BN_, st))            \
+             : (bf ? mbs::launch_grouped<BN_, 4, 4, true, 1, true>(b, a, c, n, ldc, wrows, BN_, st)              \
+                   : mbs::launch_grouped<BN_, 4, 4, false, 1, true>(b, a, c, n, ldc, wrows, BN_, st))
   if (max_tok <= 16) MXQ_GRP(16);
   if (max_tok <= 32) MXQ_GRP(32);
   MXQ_GRP(64);

@@ -135,9 +135,10 @@ def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dt
                              check: bool = True) -> list:
     """``[matmul_quantized(a, b) for a, b in zip(aqs, bqs)]`` for MoE-style
     expert GEMMs (SURVEY section 8 d config 5): ``aqs[g]`` the tokens routed
-    to expert g (at most 64 rows for the grouped kernel), ``bqs[g]`` that
+    to expert g (at most 128 rows for the grouped kernel), ``bqs[g]`` that
     expert's weights, all of one shape.  MBS / E8M0 pairs of one variant pair
-    run as one launch of the swap-AB MBS kernel per 64 experts
+    run as one launch of the MBS kernel per 64 experts (swap-AB up to 64
+    tokens, direct 128-row tiles up to 128)
     (csrc/gemm_mbs.cu ``k_gemm_mbs_grouped``); other pairs fall back to one
     launch per expert.  Tolerance parity as ``matmul_quantized``."""
     aqs, bqs = list(aqs), list(bqs)

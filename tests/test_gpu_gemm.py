@@ -219,6 +219,8 @@ def test_quantize_matmul_fused_repeated_and_nonfinite():
     ([33, 64, 17], 384, 1024, "mbs_d", "mbs_s", torch.bfloat16),
     ([8] * 70, 256, 512, "mbs_d", "mbs_s", torch.float32),            # 70 groups: two launches
     ([2, 9], 512, 1024, "mx16_oas", "mbs_s", torch.float32),          # non-MBS weights
+    ([100, 128, 65], 640, 2880, "mbs_d", "mbs_s", torch.float32),     # direct form (65-128 tokens)
+    ([128] * 3, 384, 1024, "mbs_d", "mbs_s", torch.bfloat16),
     ([4, 4], 512, 1024, "nvfp4", "nvfp4", torch.float32),             # per-group fallback
 ])
 def test_grouped_expert_gemm_matches_reference(toks, n, k, wv, av, out_dtype):

@@ -136,14 +136,14 @@ def c5():
                 res.append({"layer": lname, "arm": arm, "m": m, "n": n, "k": k, "us": round(ms * 1e3, 2),
                             "weight_gbs": round(wbytes / (ms * 1e-3) / 1e9, 1),
                             "tflops": round(2.0 * m * n * k / (ms * 1e-3) / 1e12, 2)})
-    # grouped: all 64 experts of a layer in one launch (tokens per expert <= 64)
+    # grouped: all 64 experts of a layer in one launch (tokens per expert <= 128)
     grouped = []
     for lname, n, k in (("gate_up", 5760, 2880), ("down", 2880, 2880)):
         E = 64
         wq = [M.quantize_tensor((torch.randn(n, k, device=dev, generator=g) * 0.02).to(bf16),
                                 M.SchemeConfig(V.MBS_D)) for _ in range(E)]
         wbytes = E * (n * k * (0.5 + 1 / 16) + n * ((k + 127) // 128) * 4)
-        for m in (1, 8, 32, 64):
+        for m in (1, 8, 32, 64, 128):
             aq = [M.quantize_tensor(torch.randn(m, k, device=dev, generator=g).to(bf16), M.SchemeConfig(V.MBS_S))
                   for _ in range(E)]
             fn = lambda i: M.matmul_quantized_grouped(aq, wq, out_dtype=bf16, check=False)
@@ -155,8 +155,9 @@ def c5():
         del wq
     return {"config": "C5 GPT-OSS-120B expert GEMMs, one expert per launch cycling over 16 experts (weights > L2)",
             "rows": res, "grouped_rows": grouped,
-            "grouped_note": "matmul_quantized_grouped: the 64 experts' GEMMs in one launch of the swap-AB MBS kernel "
-                            "(one CTA pair per 128 weight rows of an expert), weights streamed from HBM once",
+            "grouped_note": "matmul_quantized_grouped: the 64 experts' GEMMs in one launch of the MBS kernel -- swap-AB "
+                            "(one CTA pair per 128 weight rows of an expert) up to 64 tokens, direct 128x192 tiles "
+                            "up to 128 -- weights streamed from HBM once",
             "note": "HBM-bound on weights: compare weight_gbs with the measured 6.55 TB/s copy bandwidth; "
                     "one 128-row M tile per launch leaves most SMs idle at these N (no split-K yet)"}
 
