@@ -218,9 +218,14 @@ __device__ __forceinline__ uint32_t e2m1x2(float lo, float hi) {
 MXQ_HD double e4m3_decode(uint32_t c) {
   uint32_t e = (c >> 3) & 15u, m = c & 7u;
   double v;
-  if (e == 0) v = (double)m * 0.001953125;  // m * 2^-9
-  else if (e == 15 && m == 7) v = NAN;
-  else v = ldexp((double)(8 + m), (int)e - 10);
+  if (e == 0) {
+    v = (double)m * 0.001953125;  // m * 2^-9
+  } else if (e == 15 && m == 7) {
+    v = NAN;
+  } else {  // (8 + m) * 2^(e - 10) = 1.m * 2^(e - 7), built from its bit pattern (exact)
+    const uint64_t bits = ((uint64_t)(e - 7 + 1023) << 52) | ((uint64_t)m << 49);
+    memcpy(&v, &bits, sizeof(v));
+  }
   return (c & 0x80u) ? -v : v;
 }
 
@@ -235,12 +240,18 @@ MXQ_HD uint32_t e4m3_code_f64(double r) {
     double q = rint(r * 512.0);
     return (uint32_t)q;
   }
-  int e;
-  double fr = frexp(r, &e);          // r = fr * 2^e, fr in [0.5, 1)
-  double m = rint((fr * 2.0 - 1.0) * 8.0);  // exact scaling, RNE
-  int E = e - 1 + 7;                  // biased exponent of 1.xxx * 2^(e-1)
-  if (m >= 8.0) { m = 0.0; E += 1; }
-  uint32_t code = ((uint32_t)E << 3) | (uint32_t)m;
+  // normal range [2^-6, 448): RNE of the 52-bit fraction to 3 bits on the f64
+  // bit pattern (== rint((fr * 2 - 1) * 8) with frexp, without the library calls)
+  uint64_t bits;
+  memcpy(&bits, &r, sizeof(bits));
+  const int e = (int)((bits >> 52) & 0x7ffu) - 1023;  // r = 1.f * 2^e, e in [-6, 8]
+  const uint64_t frac = bits & ((1ull << 52) - 1);
+  uint32_t m = (uint32_t)(frac >> 49);
+  const uint64_t rem = frac & ((1ull << 49) - 1), half = 1ull << 48;
+  if (rem > half || (rem == half && (m & 1u))) ++m;
+  int E = e + 7;
+  if (m >= 8u) { m = 0u; E += 1; }
+  const uint32_t code = ((uint32_t)E << 3) | m;
   return code > 0x7Eu ? 0x7Eu : code;
 }
 
