@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
                                                            double* __restrict__ ws, uint32_t* __restrict__ status) {
   __shared__ Range s_leaf[QS_MAXLEAF];
   __shared__ double s_la[QS_MAXLEAF], s_lb[QS_MAXLEAF];
-  __shared__ double s_sq[QS_WARPS][2][128];
+  __shared__ double s_sq[QS_WARPS][2][2][128];  // [warp][leaf slot][signal/error][element]
   __shared__ int s_nl;
   __shared__ unsigned long long s_cnt[2];
   __shared__ Range s_stack[64];
@@ -146,100 +146,112 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   const uint32_t ucols = (uint32_t)cols;
   const int bs_shift = has_q ? (q.block_size == 32 ? 5 : 4) : 4;
   const uint32_t umacro = has_q && q.mant ? (uint32_t)q.macro_size : 1u;
-  for (int li = warp; li < nl; li += QS_WARPS) {
-    const Range lf = s_leaf[li];
-    const int64_t row0 = lf.s / cols;
-    const uint32_t c0 = (uint32_t)(lf.s - row0 * cols);
-    // A lane's 4 elements (p0..p0+3) lie in one row and one 16-block: leaves
-    // start at multiples of 8 and rows are multiples of 16 long.  Row, block,
-    // scale, mantissa and the two dequantisation quotients are computed once
-    // per lane per leaf (the first version spent ~220 instructions per element
-    // on per-element index math and divisions).
-    const int p0 = 4 * lane;
-    double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
-    if (p0 < lf.n) {
-      const uint32_t cc = c0 + (uint32_t)p0;
-      const uint32_t dr = ucols >= 128u ? (cc >= ucols ? 1u : 0u) : cc / ucols;
-      const int64_t r = row0 + dr;
-      const uint32_t c = cc - dr * ucols;
-      float xv[4];
-      uint32_t codes4 = 0x1111u;  // (dense recon: no flush statistics)
-      if (has_q) {
-        const uint8_t* cp = q.codes + r * q.codes_ld + (c >> 1);
-        codes4 = (uint32_t)cp[0] | ((uint32_t)cp[1] << 8);
-        const uint32_t sc = q.scales[r * q.scales_ld + (c >> bs_shift)];
-        if (q.variant == NVFP4) {
-          bad |= ((sc & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
+  // Two leaves per warp iteration: their element loads overlap, and the two
+  // leaves' numpy-order accumulator chains run side by side (lanes 0-15 on
+  // leaf t = 0, lanes 16-31 on t = 1) -- the chains, not the loads, bound
+  // this kernel.
+  for (int li = warp; li < nl; li += 2 * QS_WARPS) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) xv[j] = deq_nvfp4((codes4 >> (4 * j)) & 15u, sc, st);
-        } else {
-          bad |= (sc == 255u) ? ST_BAD_E8M0 : 0u;
-          const uint32_t m8 = q.mant ? q.mant[r * q.mant_ld + c / umacro] : 0u;
-          if (sc >= 4u && sc <= 250u) {
-            // exact: every magnitude is RN(1/f) or RN(1.5/f) times a power of
-            // two (see k_dequantize)
-            float u = 1.0f, v = 1.5f;
-            if (q.mant) {
-              const float f = mbs_factor(m8);
-              u = __fdiv_rn(1.0f, f);
-              v = __fdiv_rn(1.5f, f);
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t code = (codes4 >> (4 * j)) & 15u, idx = code & 7u;
-              const float base = ((idx & 1u) && idx > 1u) ? v : u;
-              const float mag =
-                  idx ? base * __uint_as_float((uint32_t)((int)(idx >> 1) - 1 + (int)sc) << 23) : 0.0f;
-              xv[j] = (code & 8u) ? -mag : mag;
-            }
+    for (int t = 0; t < 2; ++t) {
+      const int lj = li + t * QS_WARPS;
+      if (lj >= nl) break;
+      const Range lf = s_leaf[lj];
+      const int64_t row0 = lf.s / cols;
+      const uint32_t c0 = (uint32_t)(lf.s - row0 * cols);
+      // A lane's 4 elements (p0..p0+3) lie in one row and one 16-block: leaves
+      // start at multiples of 8 and rows are multiples of 16 long.  Row, block,
+      // scale, mantissa and the two dequantisation quotients are computed once
+      // per lane per leaf (the first version spent ~220 instructions per element
+      // on per-element index math and divisions).
+      const int p0 = 4 * lane;
+      double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (p0 < lf.n) {
+        const uint32_t cc = c0 + (uint32_t)p0;
+        const uint32_t dr = ucols >= 128u ? (cc >= ucols ? 1u : 0u) : cc / ucols;
+        const int64_t r = row0 + dr;
+        const uint32_t c = cc - dr * ucols;
+        float xv[4];
+        uint32_t codes4 = 0x1111u;  // (dense recon: no flush statistics)
+        if (has_q) {
+          const uint8_t* cp = q.codes + r * q.codes_ld + (c >> 1);
+          codes4 = (uint32_t)cp[0] | ((uint32_t)cp[1] << 8);
+          const uint32_t sc = q.scales[r * q.scales_ld + (c >> bs_shift)];
+          if (q.variant == NVFP4) {
+            bad |= ((sc & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) xv[j] = deq_nvfp4((codes4 >> (4 * j)) & 15u, sc, st);
           } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint32_t code = (codes4 >> (4 * j)) & 15u;
-              xv[j] = q.mant ? deq_mbs(code, sc, m8) : deq_pow2(code, sc);
+            bad |= (sc == 255u) ? ST_BAD_E8M0 : 0u;
+            const uint32_t m8 = q.mant ? q.mant[r * q.mant_ld + c / umacro] : 0u;
+            if (sc >= 4u && sc <= 250u) {
+              // exact: every magnitude is RN(1/f) or RN(1.5/f) times a power of
+              // two (see k_dequantize)
+              float u = 1.0f, v = 1.5f;
+              if (q.mant) {
+                const float f = mbs_factor(m8);
+                u = __fdiv_rn(1.0f, f);
+                v = __fdiv_rn(1.5f, f);
+              }
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t code = (codes4 >> (4 * j)) & 15u, idx = code & 7u;
+                const float base = ((idx & 1u) && idx > 1u) ? v : u;
+                const float mag =
+                    idx ? base * __uint_as_float((uint32_t)((int)(idx >> 1) - 1 + (int)sc) << 23) : 0.0f;
+                xv[j] = (code & 8u) ? -mag : mag;
+              }
+            } else {
+  #pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const uint32_t code = (codes4 >> (4 * j)) & 15u;
+                xv[j] = q.mant ? deq_mbs(code, sc, m8) : deq_pow2(code, sc);
+              }
             }
           }
+        } else {
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) xv[j] = recon[r * recon_ld + c + j];
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) xv[j] = recon[r * recon_ld + c + j];
+  #pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float rv = load_ref(ref, dtype, r * ref_ld + c + j);
+          const double r64 = (double)rv;
+          const double d = __dsub_rn(r64, (double)xv[j]);
+          a4[j] = __dmul_rn(r64, r64);
+          b4[j] = __dmul_rn(d, d);
+          if (rv != 0.0f) {
+            ++nz;
+            if (((codes4 >> (4 * j)) & 7u) == 0) ++fl;
+          }
+        }
       }
-#pragma unroll
+  #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const float rv = load_ref(ref, dtype, r * ref_ld + c + j);
-        const double r64 = (double)rv;
-        const double d = __dsub_rn(r64, (double)xv[j]);
-        a4[j] = __dmul_rn(r64, r64);
-        b4[j] = __dmul_rn(d, d);
-        if (rv != 0.0f) {
-          ++nz;
-          if (((codes4 >> (4 * j)) & 7u) == 0) ++fl;
-        }
+        s_sq[warp][t][0][p0 + j] = a4[j];
+        s_sq[warp][t][1][p0 + j] = b4[j];
       }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      s_sq[warp][0][p0 + j] = a4[j];
-      s_sq[warp][1][p0 + j] = b4[j];
     }
     __syncwarp();
-    // lanes 0-7: signal accumulators r[j]; lanes 8-15: error accumulators.
+    // lane = 16 t + 8 w + j: leaf t, w = 0 signal / 1 error, accumulator j
+    const int t = lane >> 4, lj = li + t * QS_WARPS;
     double acc = 0.0;
-    if (lane < 16) {
-      const double* v = s_sq[warp][lane >> 3];
-      const int j = lane & 7;
+    if (lj < nl) {
+      const double* v = s_sq[warp][t][(lane >> 3) & 1];
+      const int j = lane & 7, ln = (int)s_leaf[lj].n;
       acc = v[j];
-      const int ln = (int)lf.n;
       for (int i = 8; i < ln; i += 8) acc = __dadd_rn(acc, v[i + j]);
     }
-    double r0 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 0), r1 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 1);
-    double r2 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 2), r3 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 3);
-    double r4 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 4), r5 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 5);
-    double r6 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 6), r7 = __shfl_sync(0xffffffffu, acc, (lane & 8) | 7);
+    const int base = lane & 24;
+    double r0 = __shfl_sync(0xffffffffu, acc, base | 0), r1 = __shfl_sync(0xffffffffu, acc, base | 1);
+    double r2 = __shfl_sync(0xffffffffu, acc, base | 2), r3 = __shfl_sync(0xffffffffu, acc, base | 3);
+    double r4 = __shfl_sync(0xffffffffu, acc, base | 4), r5 = __shfl_sync(0xffffffffu, acc, base | 5);
+    double r6 = __shfl_sync(0xffffffffu, acc, base | 6), r7 = __shfl_sync(0xffffffffu, acc, base | 7);
     const double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
                                  __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-    if (lane == 0) s_la[li] = res;
-    if (lane == 8) s_lb[li] = res;
+    if ((lane & 7) == 0 && lj < nl) {
+      if (lane & 8) s_lb[lj] = res;
+      else s_la[lj] = res;
+    }
     __syncwarp();
   }
   for (int o = 16; o > 0; o >>= 1) {
