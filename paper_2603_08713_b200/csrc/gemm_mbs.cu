@@ -63,7 +63,7 @@ struct MbsCfg {
   static constexpr int THREADS = (EPIW + 4) * 32;
   static constexpr int COLS = BN / (EPIW / 4);          // output columns per epilogue thread
   static constexpr int NRB = BN / 128 + (BN % 128 ? 1 : 0);  // 128-row SF atoms a tile can touch
-  static constexpr int STAGES = BN > 128 ? 4 : (BN > 64 ? 5 : 7);  // narrow (decode) tiles: deeper weight prefetch
+  static constexpr int STAGES = BN > 128 ? 4 : (BN > 64 ? 5 : (BN > 16 ? 7 : 10));  // narrow (decode) tiles: deeper weight prefetch
   static constexpr int STAGE_B = BN * KSTAGE / 2;
   static constexpr int SFB_BYTES = NRB * 4 * ATOM;     // NRB row blocks x 4 k-steps
   static constexpr int SIG_SLOT = (BM + BN) * 4;       // sigmaA[128] + sigmaB[BN], f32
