@@ -612,6 +612,21 @@ int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t kby
   return 0;
 }
 
+int make_sf_map(CUtensorMap* m, const uint8_t* base, int64_t n_atoms) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return set_error(ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  if ((uintptr_t)base % 16) return set_error(ERR_INVALID, "scale-factor atoms must be 16-byte aligned");
+  cuuint64_t dims[2] = {128, (cuuint64_t)n_atoms};
+  cuuint64_t strides[1] = {512};
+  cuuint32_t box[2] = {128, 4};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(ERR_INVALID, "cuTensorMapEncodeTiled failed (scale factors)");
+  return 0;
+}
+
 // Block-scaled instruction descriptor (see CUTLASS cute/arch/mma_sm100_desc.hpp
 // InstrDescriptorBlockScaled): a/b format E2M1 = 1 at [7,10)/[10,13), K-major,
 // N>>3 at [17,23), scale format at 23 (1 = UE8M0, 0 = UE4M3), M>>4 at [24,29).

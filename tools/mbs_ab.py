@@ -10,6 +10,8 @@ V = M.Variant
 SHAPES = [("qkv", 4096, 6144, 4096), ("o", 4096, 4096, 4096), ("gate_up", 4096, 28672, 4096),
           ("down", 4096, 4096, 14336), ("sq8192", 8192, 8192, 8192)]
 PAIRS = [(V.MBS_S, V.MBS_D), (V.MX16_OAS, V.MX16_OAS), (V.OCP32, V.OCP32)]
+if os.environ.get("AB_SHAPES"):
+    SHAPES = [x for x in SHAPES if x[0] in os.environ["AB_SHAPES"].split(",")]
 if len(sys.argv) > 1:
     PAIRS = [p for p in PAIRS if p[0].value in sys.argv[1].split(",")]
 
