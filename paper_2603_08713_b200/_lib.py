@@ -15,7 +15,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmxq200.so")
+LIB_PATH = os.environ.get("MXQ_LIB_PATH") or os.path.join(_HERE, "_lib", "libmxq200.so")  # (override: development A/B builds)
 
 MXQ_F32, MXQ_BF16 = 0, 1
 ERR_INVALID, ERR_NONFINITE, ERR_UNSUPPORTED, ERR_RANGE = -1, -2, -3, -4

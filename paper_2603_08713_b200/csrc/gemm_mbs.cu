@@ -42,13 +42,17 @@
 #include "tc_ptx.cuh"
 
 namespace mxq {
+constexpr int KSTEP_MBS = 64;
 namespace mbs {
 
 using namespace tc;
 
 constexpr int BM = 128;
 constexpr int KSTAGE = 256, KSTEP = 64;     // K elements per pipeline stage / per MMA
-constexpr int NSFB = 2, NSIG = 8;
+#ifndef MXQ_NSIG
+#define MXQ_NSIG 8
+#endif
+constexpr int NSFB = 2, NSIG = MXQ_NSIG;
 constexpr int ATOM = 512;                   // SF atom: 128 rows x 4 blocks of 16
 constexpr int STAGE_A = BM * KSTAGE / 2;    // 16 KB of A codes per stage
 constexpr int SFA_BYTES = 4 * ATOM;         // 4 k-steps
@@ -73,7 +77,7 @@ struct MbsCfg {
   static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
   static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
   static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG;
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + NSFB;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // + alignment slack
   // TMEM: partial buffers [0, NB*BN), SF buffers 64-aligned after them
   // (misaligned SF addresses slow the MMA, tools/microbench_mma3.cu).  Within
@@ -83,7 +87,11 @@ struct MbsCfg {
   // EPIW*32*EPI + 4*32*CTRL must fit the registers allocated at launch
   // (ptxas' per-thread count x THREADS: 96 x 640 for 16 epilogue warps,
   // 168 x 384 for 8) -- setmaxnreg.inc blocks forever otherwise
+#ifndef MXQ_NO_SETMAXNREG
   static constexpr bool SETMAXNREG = COLS > 32 && EPIW > 4;
+#else
+  static constexpr bool SETMAXNREG = false;
+#endif
   static constexpr int EPI_REGS = EPIW == 16 ? 112 : 208, CTRL_REGS = EPIW == 16 ? 32 : 48;
   static_assert(EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= (EPIW == 16 ? 96 * 640 : 168 * 384), "register pool");
   static_assert(SMEM <= 232448, "shared memory budget");
@@ -118,7 +126,6 @@ struct Params {
   QDesc qa;
   uint32_t* ready;     // slices published (zeroed before the launch)
   uint32_t* status;
-  int fused_dbg;       // development timing (MXQ_FUSED_DBG): 1 = quantize only, 2 = GEMM only
 };
 
 // Grouped launch (GPT-OSS-style expert GEMMs, SURVEY section 8 d config 5): up
@@ -203,59 +210,68 @@ __device__ __forceinline__ void reg_fence(float* v) {
 }
 
 // Fused MBS-S quantization of A: A's rows are cut into
-// slices of FQ_ROWS rows dealt round-robin to the CTAs (CTA b takes slices b,
-// b + gridDim.x, ...), so all SMs stream the activation; each warp takes
-// 32-unit row segments, four in flight, through the same sq_unit as the
-// standalone k_stream_quant, so codes / scales / mantissas / sigma are
-// bit-identical to mxq_quantize.  A finished slice is published with generic
-// stores -> proxy fence -> CTA barrier -> release add on the slice counter;
-// the TMA warp acquires the full count before its first load.
-constexpr int FQ_ROWS = 8;
+// slices of FQ_ROWS rows that the running CTAs CLAIM from a work counter
+// (p.ready[1], zeroed before the launch) FQ_CLAIM slices at a time, so all
+// SMs stream the activation; each warp takes 32-unit row segments, U in
+// flight, through the same sq_unit as the standalone k_stream_quant, so codes
+// / scales / mantissas / sigma are bit-identical to mxq_quantize.  A finished
+// batch is published with generic stores -> proxy fence -> CTA barrier ->
+// release add on the slice counter p.ready[0]; the TMA warp acquires the full
+// count before its first load.  Only CTAs that are running claim slices, so
+// the wait cannot deadlock when the grid is not fully co-resident (MPS limits,
+// green contexts, a concurrent kernel holding SMs): the running CTAs quantize
+// every slice themselves.
+constexpr int FQ_ROWS = 8, FQ_CLAIM = 2;
 #ifndef MXQ_FQ_U
 #define MXQ_FQ_U 2
 #endif
 template <int G, int THREADS>
-__device__ __forceinline__ void fused_quant_a(const Params& p, const float* sig_tab) {
+__device__ __forceinline__ void fused_quant_a(const Params& p, const float* sig_tab, uint32_t* claim_slot) {
   constexpr int NW = THREADS / 32, U = MXQ_FQ_U;
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t nblk = (uint32_t)p.K / 16, segs = (nblk + 31) / 32;
   const uint32_t nslices = (uint32_t)(p.M + FQ_ROWS - 1) / FQ_ROWS;
-  const uint32_t my_slices = nslices > blockIdx.x ? (nslices - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-  // this CTA's segments, flattened over its slices (one latency round per
-  // U segments per warp, no barrier between slices)
-  const uint32_t per_slice = FQ_ROWS * segs, nseg = my_slices * per_slice;
+  const uint32_t per_slice = FQ_ROWS * segs;
   uint32_t bad = 0, ovf = 0;
-  for (uint32_t s0 = warp; s0 < nseg; s0 += U * NW) {
-    Blk16<DT_BF16> xb[U];
-    uint32_t rr[U], kk[U];
-    bool live[U];
+  for (;;) {
+    if (threadIdx.x == 0) *claim_slot = atomicAdd(p.ready + 1, (uint32_t)FQ_CLAIM);
+    __syncthreads();
+    const uint32_t first = *claim_slot;
+    __syncthreads();
+    if (first >= nslices) break;
+    const uint32_t mine = min((uint32_t)FQ_CLAIM, nslices - first);
+    const uint32_t nseg = mine * per_slice;
+    for (uint32_t s0 = warp; s0 < nseg; s0 += U * NW) {
+      Blk16<DT_BF16> xb[U];
+      uint32_t rr[U], kk[U];
+      bool live[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t j = s0 + u * NW;
-      const uint32_t js = j / per_slice, jr = j - js * per_slice;
-      const uint32_t rl = jr / segs;
-      rr[u] = (blockIdx.x + js * gridDim.x) * FQ_ROWS + rl;
-      kk[u] = (jr - rl * segs) * 32 + lane;
-      live[u] = j < nseg && rr[u] < (uint32_t)p.M;
-      if (live[u] && kk[u] < nblk) ld_blk<DT_BF16>(p.xa, (int64_t)rr[u] * p.xa_ld + kk[u] * 16, xb[u]);
-      else zero_blk<DT_BF16>(xb[u]);
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = s0 + u * NW;
+        const uint32_t js = j / per_slice, jr = j - js * per_slice;
+        const uint32_t rl = jr / segs;
+        rr[u] = (first + js) * FQ_ROWS + rl;
+        kk[u] = (jr - rl * segs) * 32 + lane;
+        live[u] = j < nseg && rr[u] < (uint32_t)p.M;
+        if (live[u] && kk[u] < nblk) ld_blk<DT_BF16>(p.xa, (int64_t)rr[u] * p.xa_ld + kk[u] * 16, xb[u]);
+        else zero_blk<DT_BF16>(xb[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (live[u])
+          sq_unit<DT_BF16, SQ_MBS_S, G>(xb[u], kk[u] < nblk, row_out(p.qa, rr[u]), p.qa.sig_t_ld, kk[u], lane,
+                                        sig_tab, bad, ovf);
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (live[u])
-        sq_unit<DT_BF16, SQ_MBS_S, G>(xb[u], kk[u] < nblk, row_out(p.qa, rr[u]), p.qa.sig_t_ld, kk[u], lane,
-                                      sig_tab, bad, ovf);
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.ready), "r"(mine) : "memory");
+    }
   }
   if (bad) atomicOr(p.status, ST_NONFINITE);
   if (ovf) atomicOr(p.status, ST_OVERFLOW);
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-  __syncthreads();
-  if (threadIdx.x == 0 && my_slices) {
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p.ready), "r"(my_slices)
-                 : "memory");
-  }
 }
 
 __device__ __forceinline__ void wait_ready(const uint32_t* flag, uint32_t want) {
@@ -287,20 +303,21 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
   const uint32_t a_full = a_smem + OFF_BAR, a_empty = a_full + 8 * STAGES;
   const uint32_t a_tfull = a_empty + 8 * STAGES, a_tempty = a_tfull + 8 * NB;
   const uint32_t a_sfull = a_tempty + 8 * NB, a_sempty = a_sfull + 8 * NSIG;
-  const uint32_t a_tmem_slot = a_sempty + 8 * NSIG;
+  const uint32_t a_sffree = a_sempty + 8 * NSIG;  // [NSFB] TMEM SF buffer consumed (its stage's MMAs done)
+  const uint32_t a_tmem_slot = a_sffree + 8 * NSFB;
 
-  if constexpr (FUSED) if (p.fused_dbg != 2) {
+  if constexpr (FUSED) {
     // phase 1: quantize this CTA's A row blocks (sigma table in the sigma ring's space)
     float* sig_tab = reinterpret_cast<float*>(smem_raw + (a_smem - smem_u32(smem_raw)) + OFF_SIG);
     for (int i = threadIdx.x; i < 256; i += C::THREADS) sig_tab[i] = 1.0f / mbs_factor((uint32_t)i);
+    uint32_t* claim_slot = reinterpret_cast<uint32_t*>(sig_tab + 256);
     __syncthreads();
-    if (p.mac_steps == 1) fused_quant_a<4, C::THREADS>(p, sig_tab);
-    else if (p.mac_steps == 2) fused_quant_a<8, C::THREADS>(p, sig_tab);
-    else fused_quant_a<16, C::THREADS>(p, sig_tab);
+    if (p.mac_steps == 1) fused_quant_a<4, C::THREADS>(p, sig_tab, claim_slot);
+    else if (p.mac_steps == 2) fused_quant_a<8, C::THREADS>(p, sig_tab, claim_slot);
+    else fused_quant_a<16, C::THREADS>(p, sig_tab, claim_slot);
     // (the sigma ring is rewritten by bulk copies: order the generic writes first)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (p.fused_dbg == 1) return;
   }
 
   // warp index through a shuffle so ptxas knows it is warp-uniform
@@ -316,7 +333,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
   const int n_ksteps = (p.K + KSTEP - 1) / KSTEP;
   const int n_stages = (p.K + KSTAGE - 1) / KSTAGE;
   const int n_chunks = p.n_chunks, mac_steps = p.mac_steps;
-  const int cps = 4 / mac_steps;                             // chunks per 256-K stage
+  const int cps = mac_steps <= 4 ? 4 / mac_steps : 0;       // chunks per 256-K stage (split-K shapes only)
   const int spl = (n_stages + ksplit - 1) / ksplit;         // stages per K split
   // A work unit: one (128-row group, BN-column tile, K split) of the output;
   // the CTAs of a cluster take consecutive 128-row blocks of it.
@@ -331,8 +348,9 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
     r.nb = rest / groups_m;
     r.s_lo = r.split * spl;
     r.s_hi = min(r.s_lo + spl, n_stages);
-    r.c_lo = r.s_lo * cps;
-    r.c_hi = min(r.s_hi * cps, n_chunks);
+    // (K splits only when chunks tile the 256-K stages: macro 64 / 128 / 256)
+    r.c_lo = ksplit > 1 ? r.s_lo * cps : 0;
+    r.c_hi = ksplit > 1 ? min(r.s_hi * cps, n_chunks) : n_chunks;
     return r;
   };
 
@@ -349,6 +367,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
       mbar_init_a(a_sfull + 8 * b, 1);
       mbar_init_a(a_sempty + 8 * b, EPIW);
     }
+    for (int b = 0; b < NSFB; ++b) mbar_init_a(a_sffree + 8 * b, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if constexpr (!GROUPED) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmA)) : "memory");
@@ -372,8 +391,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
       // (fused: A is complete once every slice is published -- the first wave
       // of tiles covers every row block, so one wait before the loop costs
       // nothing and keeps the 32-register producer loop free of spills)
-      if constexpr (FUSED)
-        if (p.fused_dbg != 2) wait_ready(p.ready, (uint32_t)((p.M + FQ_ROWS - 1) / FQ_ROWS));
+      if constexpr (FUSED) wait_ready(p.ready, (uint32_t)((p.M + FQ_ROWS - 1) / FQ_ROWS));
       uint32_t st = 0, ph = 0, slot = 0, sph = 0;
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         const Unit U = unit_of(unit);
@@ -459,9 +477,13 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           for (; ks < kend; ++ks) {
             const uint32_t j = (uint32_t)ks & 3u;
             if (j == 0) {
-              // this stage's SF atoms -> SF buffer g % 2 (the buffer's previous
-              // readers, stage g-2's MMAs, precede these copies in the pipe)
+              // this stage's SF atoms -> SF buffer g % 2.  Its previous
+              // readers are stage g-2's MMAs: tcgen05.cp is NOT ordered after
+              // an earlier tcgen05.mma's scale-factor reads (measured: stale
+              // scales in a few column groups at the Llama qkv shape when the
+              // MMA issue runs a stage ahead), so wait for their commit.
               sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
+              if (g >= NSFB) mbar_wait_a(a_sffree + (g & (NSFB - 1)) * 8, ((g / NSFB) - 1) & 1u);
               mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
               trace_at(p, q, 10);
               tc_fence_after();
@@ -480,6 +502,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
             if (j == 3 || ks + 1 == n_ksteps) {
               if constexpr (CL == 1) tc_commit_e(a_empty + st * 8);
               else tc_commit_mc_e(a_empty + st * 8, (uint16_t)((1u << CL) - 1));
+              tc_commit_e(a_sffree + (g & (NSFB - 1)) * 8);
               ++g;
               if (++st == STAGES) st = 0;
             }
@@ -499,6 +522,14 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
     const uint32_t sig_a = a_smem + OFF_SIG + row_in_tile * 4;
     const uint32_t sig_b = a_smem + OFF_SIG + (BM + grp * COLS) * 4;
     uint32_t q = 0, lbuf = 0, ltph = 0, slot = 0, sph = 0;
+    // sigma slot read by the previous chunk, released one chunk late: the
+    // SASS scheduler hoists an mbarrier.arrive above the FMULs that consume
+    // the slot's LDS results (nothing in PTX ties them), and an LDS still in
+    // flight then reads the producer's refill (measured: sigma_B columns 24-47
+    // of the slowest warps at the Llama qkv shape).  One chunk later every
+    // FMUL of the previous fold has issued -- so every LDS has returned (in-order
+    // issue, register scoreboard) -- before the arrive can issue.
+    uint32_t pend = NSIG;
 
     for (int unit = unit0; unit < num_units; unit += unit_step) {
       const Unit U = unit_of(unit);
@@ -523,6 +554,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         tc_fence_before();
         __syncwarp();
         arrive_e(a_tempty + lbuf * 8);
+        if (pend != NSIG) arrive_e(a_sempty + pend * 8);
         if (warp == 0) trace_at(p, q, 5);
         if (++lbuf == NB) { lbuf = 0; ltph ^= 1; }
         // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
@@ -539,8 +571,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           fma2(acc[i], acc[i + 1], w0, w1, v[i], v[i + 1]);
           fma2(acc[i + 2], acc[i + 3], w2, w3, v[i + 2], v[i + 3]);
         }
-        __syncwarp();
-        arrive_e(a_sempty + slot * 8);
+        pend = slot;
         if (warp == 0) trace_at(p, q, 7);
         if (warp == EPIW - 1) trace_at(p, q, 9);
         if (++slot == NSIG) { slot = 0; sph ^= 1; }
@@ -609,6 +640,10 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           }
         }
       }
+    }
+    if (pend != NSIG) {  // (the last slot: nothing refills it, released for symmetry)
+      __syncwarp();
+      arrive_e(a_sempty + pend * 8);
     }
   }
 
@@ -1041,6 +1076,7 @@ __global__ void __launch_bounds__(Mbs2Cfg<PAIR>::THREADS, 1)
     if (warp == 0) trace_at(p, qe + c, 7);                                                         \
     MBS2_TR(5)                                                                                     \
     if (cs + 1 == cps || c + 1 == n_chunks) {                                                      \
+      reg_fence<64>(acc); /* every sigma load has returned (see mbs_body) */                       \
       __syncwarp();                                                                                \
       if (!(MXQ_MBS2_EXP & 8)) arrive_e(a_sempty + slot * 8);                                                               \
       if (++slot == NSIG2) { slot = 0; sph ^= 1; }                                                 \
@@ -1142,19 +1178,21 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   p.qa = a;
   p.ready = ready;
   p.status = status;
-  if constexpr (FUSED) {
-    static int dbg = -1;
-    if (dbg < 0) {
-      const char* d = getenv("MXQ_FUSED_DBG");
-      dbg = d ? atoi(d) : 0;
-    }
-    p.fused_dbg = dbg;
-  }
   // E2M1 x E2M1, UE8M0 scales, N = BN, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
   p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
   const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN) * ksplit;
   int clusters = num_sms() / CL;
   if (units < clusters) clusters = units;
+  if constexpr (FUSED) {
+    // test hook (MXQ_FUSED_OVERSUBSCRIBE=k): k times more CTAs than can be
+    // co-resident, to exercise the claim-based quantization phase
+    static int over = -1;
+    if (over < 0) {
+      const char* d = getenv("MXQ_FUSED_OVERSUBSCRIBE");
+      over = d ? std::max(1, atoi(d)) : 1;
+    }
+    clusters *= over;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(clusters * CL);
   cfg.blockDim = dim3(C::THREADS);
@@ -1321,23 +1359,25 @@ static int launch_grouped(const QDesc* ka, const QDesc* kb, void* const* c, int 
 
 }  // namespace mbs
 
-// MBS pair on the tcgen05 path: macro sizes 64, 128, 256 (chunks never
-// straddle a 256-K stage; other sizes take the first-generation kernel).
+// MBS pair on the tcgen05 path: any macro size that is a multiple of the
+// 64-K MMA step (a chunk may straddle 256-K stages; K splits need 64 / 128 /
+// 256).  Other macro sizes have no chunk boundary on an MMA step: the exact
+// CUDA-core kernel takes them (gemm.py tc_supported).
 bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
   const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
   if (!ma && !mb) return false;
   if (a.variant == NVFP4 || b.variant == NVFP4) return false;  // (an MBS operand makes the SF layout block-16)
   const int macro = ma ? a.macro_size : b.macro_size;
   if (ma && mb && a.macro_size != b.macro_size) return false;
-  return macro == 64 || macro == 128 || macro == 256;
+  return macro % KSTEP_MBS == 0;
 }
 
 // Split count for few-tile shapes: split K at stage boundaries so every SM
 // streams weights (decode-like M <= 64 only: at M = 128 the f32 partial
 // traffic and the reduce cost more than the parallelism wins, 18 vs 21 us on
 // the GPT-OSS gate_up shape, profiles/configs_r01.json).
-static int choose_ksplit(int rows_small, int base_clusters, int slots, int n_stages) {
-  if (rows_small > 64 || 2 * base_clusters > slots || n_stages < 4) return 1;
+static int choose_ksplit(int rows_small, int base_clusters, int slots, int n_stages, int macro) {
+  if (rows_small > 64 || 2 * base_clusters > slots || n_stages < 4 || 256 % macro) return 1;
   int ks = std::min(slots / base_clusters, n_stages / 2);
   const int spl = (n_stages + ks - 1) / ks;
   return (n_stages + spl - 1) / spl;  // no empty split
@@ -1348,8 +1388,11 @@ static int launch_shape(const QDesc& ka, const QDesc& kb, void* c, bool bf, int6
   const int tiles_m = (int)((ka.rows + mbs::BM - 1) / mbs::BM), tiles_n = (int)((kb.rows + BN - 1) / BN);
   const int n_stages = (int)((ka.cols + mbs::KSTAGE - 1) / mbs::KSTAGE);
   // one 128-row block: no pairing across M, so no cluster (its second CTA would idle)
-  const int CL = tiles_m >= 2 ? 2 : 1;
-  int ksplit = choose_ksplit(rows_small, ((tiles_m + CL - 1) / CL) * tiles_n, num_sms() / CL, n_stages);
+  static int force_cl1 = -1;
+  if (force_cl1 < 0) force_cl1 = getenv("MXQ_MBS_CL1") ? 1 : 0;  // development A/B
+  const int CL = (tiles_m >= 2 && !force_cl1) ? 2 : 1;
+  const int macro = (ka.variant == MBS_S || ka.variant == MBS_D) ? ka.macro_size : kb.macro_size;
+  int ksplit = choose_ksplit(rows_small, ((tiles_m + CL - 1) / CL) * tiles_n, num_sms() / CL, n_stages, macro);
   // split-K partials: a stream-ordered allocation per call (pool-cached,
   // graph-capturable, private to this launch -- no workspace shared between
   // streams); without one the launch runs unsplit
@@ -1385,21 +1428,16 @@ int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_
     if (a.rows <= 32) return launch_shape<32, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
     return launch_shape<64, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
   }
-  // prefill shapes: the 128 x 128 double-buffered kernel (clusters of 4 along M
-  // when the 128-row blocks divide evenly, else 2; a single block runs alone)
-  const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM);
-  static int force_cl = -1;
-  if (force_cl < 0) {
-    const char* e = getenv("MXQ_MBS_CL");
-    force_cl = e ? atoi(e) : 0;
+  // prefill shapes: 128 x 192 tiles (the experimental 128 x 128 kernel only
+  // with MXQ_MBS_KERNEL=2, development A/B)
+  static int kern2 = -1;
+  if (kern2 < 0) {
+    const char* e = getenv("MXQ_MBS_KERNEL");
+    kern2 = (e && atoi(e) == 2) ? 1 : 0;
   }
-  if (force_cl != 192 && a.rows > 64) {
-    int cl = tiles_m % 4 == 0 ? 4 : (tiles_m >= 2 ? 2 : 1);
-    cl = tiles_m >= 2 ? 2 : 1;
-#ifdef MXQ_MBS2_FORCE_CL1
-    cl = 1;
-#endif
-    if (cl == 2) return bf ? mbs::launch2<true, true>(a, b, c, ldc, st) : mbs::launch2<true, false>(a, b, c, ldc, st);
+  if (kern2 && a.rows > 64) {
+    const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM);
+    if (tiles_m >= 2) return bf ? mbs::launch2<true, true>(a, b, c, ldc, st) : mbs::launch2<true, false>(a, b, c, ldc, st);
     return bf ? mbs::launch2<false, true>(a, b, c, ldc, st) : mbs::launch2<false, false>(a, b, c, ldc, st);
   }
   return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
@@ -1442,8 +1480,9 @@ int launch_gemm_mbs_grouped(const QDesc* a, const QDesc* b, int n, void* const* 
 }
 
 bool gemm_mbs_fusable(const QDesc& a, const QDesc& b, int x_dtype) {
+  // (the in-kernel quantizer assigns power-of-two macros to lane groups)
   return x_dtype == DT_BF16 && a.variant == MBS_S && gemm_mbs_supported(a, b) && !(a.rows <= 64 && b.rows >= 256) &&
-         a.scales_mma && a.sig_t;
+         (a.macro_size == 64 || a.macro_size == 128 || a.macro_size == 256) && a.scales_mma && a.sig_t;
 }
 
 // Fused MBS-S activation quantization + MBS GEMM in one launch (callers check
@@ -1452,8 +1491,8 @@ int launch_gemm_mbs_fused(const void* x, int64_t x_ld, const QDesc& a, const QDe
                           int64_t ldc, uint32_t* status, cudaStream_t st) {
   const bool bf = c_dtype == MXQ_BF16;
   const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM);
-  uint32_t* ready = status + 2;  // the call's own scratch word: nothing shared between launches
-  const cudaError_t e = cudaMemsetAsync(ready, 0, sizeof(uint32_t), st);
+  uint32_t* ready = status + 2;  // the call's own scratch words (published, claimed): nothing shared between launches
+  const cudaError_t e = cudaMemsetAsync(ready, 0, 2 * sizeof(uint32_t), st);
   if (e != cudaSuccess) return set_cuda_error(e);
   if (tiles_m >= 2)
     return bf ? mbs::launch<192, 2, 16, true, 2, false, true>(a, b, c, ldc, 1, nullptr, st, x, x_ld, ready, status)

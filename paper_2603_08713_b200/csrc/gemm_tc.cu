@@ -764,7 +764,13 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
   const bool nva = a.variant == NVFP4, nvb = b.variant == NVFP4;
   if (nva != nvb) return set_error(ERR_UNSUPPORTED, "UE8M0 x UE4M3 operand pair has no block-scaled MMA form");
   const bool mbs = (a.variant == MBS_S || a.variant == MBS_D || b.variant == MBS_S || b.variant == MBS_D);
-  const bool sf32 = (a.block_size == 32 && b.block_size == 32) && a.sf_kpad * 32 == b.sf_kpad * 32;
+  // scale-factor atom layout of each operand: sf_kpad = round_up(K, 256) / sf_block
+  const int64_t kp16 = (a.cols + 255) / 256 * 16, kp32 = kp16 / 2;
+  const bool a32 = a.sf_kpad == kp32 && a.block_size == 32, b32 = b.sf_kpad == kp32 && b.block_size == 32;
+  if ((!a32 && a.sf_kpad != kp16) || (!b32 && b.sf_kpad != kp16))
+    return set_error(ERR_INVALID, "scale-factor layout does not match a 16- or 32-element block");
+  const bool sf32 = a32 && b32;
+  if (!sf32 && (a32 || b32)) return set_error(ERR_INVALID, "operands disagree on the scale-factor block");
   if (a.rows > (1 << 30) || b.rows > (1 << 30) || a.cols > (1 << 30)) return set_error(ERR_UNSUPPORTED, "shape too large");
   if (mbs) {
     const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
@@ -772,9 +778,8 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
     const int macro = ma ? a.macro_size : b.macro_size;
     if (macro % KSTEP) return set_error(ERR_UNSUPPORTED, "macro_size must be a multiple of 64 on the tcgen05 path");
     if (ma && mb && a.macro_size != b.macro_size) return set_error(ERR_UNSUPPORTED, "operands disagree on macro_size");
-    if (gemm_mbs_supported(a, b) && !mbs_v1()) return launch_gemm_mbs(a, b, c, c_dtype, ldc, st);
-    if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<128, 4, 3, false, true, true, 1>(a, b, c, ldc, true, st) : launch_variant<128, 4, 3, false, true, true, 2>(a, b, c, ldc, true, st));
-    return (cluster_size() == 1 ? launch_variant<128, 4, 3, false, true, false, 1>(a, b, c, ldc, true, st) : launch_variant<128, 4, 3, false, true, false, 2>(a, b, c, ldc, true, st));
+    if (!gemm_mbs_supported(a, b)) return set_error(ERR_UNSUPPORTED, "MBS pair not supported on the tcgen05 path");
+    return launch_gemm_mbs(a, b, c, c_dtype, ldc, st);
   }
   if (sf32) {
     if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, false, true, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, false, true, 2>(a, b, c, ldc, true, st));

@@ -17,6 +17,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
+#include <memory>
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
@@ -376,10 +378,15 @@ __device__ __forceinline__ double pw_sum_smem_t(const double* base, int64_t s, i
 
 __device__ double pw_sum_smem(const double* base, int64_t s, int64_t n) { return pw_sum_smem_t<3>(base, s, n); }
 
-__constant__ uint8_t c_cands[256];
-// LUT mode table (src/quantize.py:482-504): [regime][candidate][bin] fp16
-// values widened to f32 (exact).
-__constant__ float c_lut[2][16][64];
+// MBS-D candidate bytes and (LUT mode) the error table (src/quantize.py:482-504:
+// [regime][candidate][bin] fp16 values widened to f32, exact), passed BY VALUE
+// as a __grid_constant__ kernel parameter: every launch carries its own copy,
+// so concurrent quantize calls on different streams cannot see each other's
+// candidates (no process-global __constant__ symbol is written).
+struct MbsdTables {
+  uint8_t cands[256];
+  float lut[2][16][64];
+};
 
 // LUT=false: exact SSE search (src/quantize.py:438-461).
 // LUT=true : table-estimated cost sum(x^2 * T[v]) (src/quantize.py:507-542),
@@ -387,7 +394,8 @@ __constant__ float c_lut[2][16][64];
 template <bool LUT>
 __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __restrict__ x, int dtype, int64_t x_ld,
                                                                  QDesc q, MacroGeom g, int n_cand, int augment,
-                                                                 uint32_t* __restrict__ status) {
+                                                                 uint32_t* __restrict__ status,
+                                                                 const __grid_constant__ MbsdTables tab) {
   __shared__ double s_sq[MBSD_THREADS * MBSD_STRIDE];
   const int lane = threadIdx.x & 31;
   const int sub = lane & (g.G - 1);
@@ -419,7 +427,7 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
     double best_sse = 0.0;
     uint32_t best_m8 = 0;
     for (int t = 0; t < n_trials; ++t) {
-      const uint32_t m8 = t < n_cand ? (uint32_t)c_cands[t] : m8_static;
+      const uint32_t m8 = t < n_cand ? (uint32_t)tab.cands[t] : m8_static;
       const float f = mbs_factor(m8);
       // quantise: y = x*f, OAS scale, codes
       float y[16];
@@ -441,11 +449,11 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
           if (vv < 1.0) {
             long long b = (long long)__dmul_rn(vv, 64.0);
             b = b < 0 ? 0 : (b > 63 ? 63 : b);
-            tv = (double)c_lut[0][t][b];
+            tv = (double)tab.lut[0][t][b];
           } else {
             long long b = (long long)__ddiv_rn(__dmul_rn(__dsub_rn(vv, 1.0), 64.0), 7.0);
             b = b < 0 ? 0 : (b > 63 ? 63 : b);
-            tv = (double)c_lut[1][t][b];
+            tv = (double)tab.lut[1][t][b];
           }
           mine[i] = active ? __dmul_rn(__dmul_rn(x64, x64), tv) : 0.0;
         }
@@ -625,13 +633,14 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       } else {
         if (mbs_mode != 0) return set_error(ERR_INVALID, "mbs_mode='lut' runs through mxq_quantize_mbs_lut");
         if (n_cand < 1 || n_cand > 256) return set_error(ERR_INVALID, "candidate count out of range");
-        cudaError_t e = cudaMemcpyToSymbolAsync(c_cands, cand, (size_t)n_cand, 0, cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return set_cuda_error(e);
+        if (!cand) return set_error(ERR_INVALID, "null candidate list");
+        std::unique_ptr<MbsdTables> tab(new MbsdTables());
+        memcpy(tab->cands, cand, (size_t)n_cand);
         const int64_t gpb = MBSD_THREADS / g.G;
         int64_t blocks = (ngroups + gpb - 1) / gpb;
         int64_t cap = (int64_t)num_sms() * 16;
         k_quantize_mbs_d<false><<<(int)(blocks < cap ? blocks : cap), MBSD_THREADS, 0, st>>>(
-            x, dtype, x_ld, q, g, n_cand, augment, status);
+            x, dtype, x_ld, q, g, n_cand, augment, status, *tab);
       }
       break;
     }
@@ -665,15 +674,15 @@ int launch_quantize_lut(const void* x, int dtype, int64_t x_ld, const QDesc& q, 
   g.G = macro_lanes(q.macro_size);
   g.nmac = (q.cols + q.macro_size - 1) / q.macro_size;
   if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_cands, cand, 16, 0, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemcpyToSymbolAsync(c_lut, lut, sizeof(float) * 2 * 16 * 64, 0, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return set_cuda_error(e);
+  std::unique_ptr<MbsdTables> tab(new MbsdTables());
+  memcpy(tab->cands, cand, 16);
+  memcpy(tab->lut, lut, sizeof(tab->lut));
   const int64_t ngroups = q.rows * g.nmac;
   const int64_t gpb = MBSD_THREADS / g.G;
   int64_t blocks = (ngroups + gpb - 1) / gpb;
   int64_t cap = (int64_t)num_sms() * 16;
   k_quantize_mbs_d<true><<<(int)(blocks < cap ? blocks : cap), MBSD_THREADS, 0, st>>>(x, dtype, x_ld, q, g, 16, 0,
-                                                                                     status);
+                                                                                     status, *tab);
   return check_launch();
 }
 

@@ -109,26 +109,64 @@ def matmul_quantized(aq: QuantizedTensor, bq: QuantizedTensor, cfg: TileConfig =
     _validate_chunking(bq, cfg.t_k, "b")
     m, n = aq.shape[0], bq.shape[0]
     dev = aq.codes.device
-    status = torch.zeros(4, dtype=torch.int32, device=dev)
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("out_dtype must be float32 or bfloat16")
+    if out is not None:
+        _check_out(out, m, n, out_dtype, dev)
     stream = _lib.stream_handle()
     L = _lib.lib()
     if exact or not tc_supported(aq, bq):
         c = torch.empty((m, n), dtype=torch.float32, device=dev)
+        status = torch.zeros(4, dtype=torch.int32, device=dev)
         qa, qb = aq.qt(), bq.qt()
         _lib.check(L.mxq_gemm_exact(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), n, status.data_ptr(), stream),
                    "matmul_quantized(exact)")
         if check:
             _lib.raise_on_status(status)
+        if out is not None:
+            out.copy_(c)
+            return out
         return c if out_dtype == torch.float32 else c.to(out_dtype)
-    if out_dtype not in (torch.float32, torch.bfloat16):
-        raise ValueError("out_dtype must be float32 or bfloat16")
+    if check:
+        _check_scale_codes(aq)
+        _check_scale_codes(bq)
     c = out if out is not None else torch.empty((m, n), dtype=out_dtype, device=dev)
     sfb = _sf_block(aq, bq)
     qa, qb = aq.gemm_qt(sfb), bq.gemm_qt(sfb)
     dt = _lib.MXQ_BF16 if out_dtype == torch.bfloat16 else _lib.MXQ_F32
-    _lib.check(L.mxq_gemm(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), dt, c.stride(0), status.data_ptr(),
-                          stream), "matmul_quantized")
+    # (the tcgen05 kernels report nothing through the status word: no buffer)
+    _lib.check(L.mxq_gemm(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), dt, c.stride(0), None, stream),
+               "matmul_quantized")
     return c
+
+
+def _check_out(out: torch.Tensor, m: int, n: int, out_dtype: torch.dtype, dev) -> None:
+    """``out=`` must be exactly the result tensor the call would allocate
+    (shape, dtype, device, unit column stride): the kernels write through
+    its pointer and row pitch."""
+    if not isinstance(out, torch.Tensor) or tuple(out.shape) != (m, n):
+        raise ValueError(f"out must have shape {(m, n)}, got {getattr(out, 'shape', None)}")
+    if out.dtype != out_dtype:
+        raise ValueError(f"out has dtype {out.dtype} but out_dtype is {out_dtype}")
+    if out.device != dev:
+        raise ValueError(f"out is on {out.device}, the operands on {dev}")
+    if out.stride(1) != 1 or out.stride(0) < n:
+        raise ValueError("out must have unit column stride and a row pitch >= n")
+
+
+def _check_scale_codes(q: QuantizedTensor) -> None:
+    """The reference's corrupt-scale ValueError (src/quantize.py:228-241),
+    checked once per tensor: the quantizers never write an E8M0 255 or an
+    E4M3 NaN byte, so only tensors built or edited by the caller are scanned."""
+    c = q._cache
+    if c.get("scales_ok") or "status" in c:
+        return
+    if q.variant is Variant.NVFP4:
+        if bool(((q.e4m3_scales & 0x7F) == 0x7F).any()):
+            raise ValueError("corrupt block scale: E4M3 NaN code")
+    elif bool((q.block_scales == 255).any()):
+        raise ValueError("corrupt block scale: E8M0 code 255 is reserved")
+    c["scales_ok"] = True
 
 
 def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dtype: torch.dtype = torch.float32,
@@ -154,8 +192,10 @@ def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dt
         _validate_chunking(bq, cfg.t_k, "b")
     if out_dtype not in (torch.float32, torch.bfloat16):
         raise ValueError("out_dtype must be float32 or bfloat16")
-    if not all(tc_supported(aq, bq) for aq, bq in zip(aqs, bqs)) or any(
-            aq.variant is Variant.NVFP4 for aq in aqs):
+    # the grouped kernel takes MBS pairs (block-16 scale layout); anything else
+    # runs expert by expert through matmul_quantized
+    if not all(tc_supported(aq, bq) and (aq.mbs_mantissas is not None or bq.mbs_mantissas is not None)
+               and Variant.NVFP4 not in (aq.variant, bq.variant) for aq, bq in zip(aqs, bqs)):
         return [matmul_quantized(aq, bq, cfg, out_dtype=out_dtype, check=check) for aq, bq in zip(aqs, bqs)]
     dev = aqs[0].codes.device
     outs = [torch.empty((aq.shape[0], n), dtype=out_dtype, device=dev) for aq in aqs]
@@ -189,7 +229,11 @@ def quantize_matmul(a, bq: QuantizedTensor, cfg: SchemeConfig = SchemeConfig(Var
     cfg = cfg if isinstance(cfg, SchemeConfig) else SchemeConfig(cfg)
     fusable = (cfg.variant is Variant.MBS_S and bq.variant in (Variant.MBS_S, Variant.MBS_D, Variant.MX16,
                                                                 Variant.MX16_OAS, Variant.OCP32)
-               and isinstance(a, torch.Tensor) and a.dtype == torch.bfloat16 and a.is_cuda)
+               and isinstance(a, torch.Tensor) and a.dtype == torch.bfloat16 and a.is_cuda
+               # the pair must be one the tcgen05 MBS kernel takes (else: two calls,
+               # and matmul_quantized picks the path, as for any other pair)
+               and cfg.macro_size in (64, 128, 256)
+               and (bq.mbs_mantissas is None or bq.macro_size == cfg.macro_size))
     if not fusable:
         aq = quantize_tensor(a, cfg, check=check)
         return matmul_quantized(aq, bq, tile, out_dtype=out_dtype, out=out, check=check), aq
@@ -208,6 +252,8 @@ def quantize_matmul(a, bq: QuantizedTensor, cfg: SchemeConfig = SchemeConfig(Var
     bufs = _q._Outputs(Variant.MBS_S, rows, cols, 16, macro, x.device, True)
     qa = bufs.qt(Variant.MBS_S, rows, cols, 16, macro)
     n = bq.shape[0]
+    if out is not None:
+        _check_out(out, rows, n, out_dtype, x.device)
     c = out if out is not None else torch.empty((rows, n), dtype=out_dtype, device=x.device)
     qb = bq.gemm_qt(16)  # (an MBS-S A makes the pair block-16)
     dtc = _lib.MXQ_BF16 if out_dtype == torch.bfloat16 else _lib.MXQ_F32

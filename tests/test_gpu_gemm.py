@@ -94,8 +94,8 @@ def test_tk_validation_like_reference():
 
 @pytest.mark.parametrize("macro", [64, 128, 256, 512])
 def test_tc_gemm_mbs_macro_sizes(macro):
-    """The 192-column MBS kernel takes macros 64/128/256 (512 runs the
-    first-generation kernel); partial last macro at K = 2880."""
+    """The 192-column MBS kernel at macros 64 / 128 / 256 / 512 (512: chunks
+    straddle the 256-K stages); partial last macro at K = 2880."""
     rng = np.random.Generator(np.random.PCG64(11 + macro))
     for (m, n, k) in [(200, 500, 1024), (130, 384, 2880)]:
         a = rng.standard_t(4, (m, k)).astype(np.float32)
@@ -243,3 +243,31 @@ def test_grouped_expert_gemm_matches_reference(toks, n, k, wv, av, out_dtype):
             single = M.matmul_quantized(aq, bq, out_dtype=torch.float32).cpu().numpy()
             _check(single, want, bound, ("single", i))
             assert np.allclose(got, single, rtol=2 ** -7, atol=1e-6 * np.abs(single).max()), i
+
+
+def test_quantize_matmul_fused_not_co_resident():
+    """The fused launch must not rely on all of its CTAs being co-resident
+    (ADVICE: MPS limits, green contexts, a concurrent kernel holding SMs).
+    MXQ_FUSED_OVERSUBSCRIBE=4 launches 4x more CTAs than fit on the GPU;
+    the quantization slices are claimed by running CTAs only, so the launch
+    completes and matches the two-call result bit for bit.  (Subprocess: the
+    hook is read once per process; a hang fails through the timeout.)"""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, paper_2603_08713_b200 as M\n"
+        "g = torch.Generator(device='cuda').manual_seed(3)\n"
+        "a = torch.randn(1024, 2048, device='cuda', generator=g).to(torch.bfloat16)\n"
+        "w = (torch.randn(2304, 2048, device='cuda', generator=g) * 0.02).to(torch.bfloat16)\n"
+        "wq = M.quantize_tensor(w, M.SchemeConfig(M.Variant.MBS_D))\n"
+        "c, aq = M.quantize_matmul(a, wq)\n"
+        "c2 = M.matmul_quantized(M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S)), wq)\n"
+        "torch.cuda.synchronize()\n"
+        "assert torch.equal(c, c2)\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MXQ_FUSED_OVERSUBSCRIBE="4", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]

@@ -1,7 +1,8 @@
 """One warm launch of each hot kernel for ncu captures (development aid):
 quantize (MBS_S, MX16_OAS, NVFP4) on a 4096x4096 bf16 activation and the
 tcgen05 GEMM (MBS-H, OCP32, MX16_OAS) at the given size."""
-import sys
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2603_08713_b200 as M
 
