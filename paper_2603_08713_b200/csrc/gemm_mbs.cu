@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <type_traits>
 
 #include "mxq_arith.cuh"
 #include "mxq_internal.h"
@@ -521,15 +522,14 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
     const int row_in_tile = quad * 32 + lane;
     const uint32_t sig_a = a_smem + OFF_SIG + row_in_tile * 4;
     const uint32_t sig_b = a_smem + OFF_SIG + (BM + grp * COLS) * 4;
-    uint32_t q = 0, lbuf = 0, ltph = 0, slot = 0, sph = 0;
-    // sigma slot read by the previous chunk, released one chunk late: the
+    uint32_t q = 0;  // chunks consumed by this warp (all units)
+    // The sigma slot read by the previous chunk is released one chunk late: the
     // SASS scheduler hoists an mbarrier.arrive above the FMULs that consume
     // the slot's LDS results (nothing in PTX ties them), and an LDS still in
     // flight then reads the producer's refill (measured: sigma_B columns 24-47
     // of the slowest warps at the Llama qkv shape).  One chunk later every
     // FMUL of the previous fold has issued -- so every LDS has returned (in-order
     // issue, register scoreboard) -- before the arrive can issue.
-    uint32_t pend = NSIG;
 
     for (int unit = unit0; unit < num_units; unit += unit_step) {
       const Unit U = unit_of(unit);
@@ -538,29 +538,36 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
       float acc[COLS];
 #pragma unroll
       for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
-#pragma unroll 1
-      for (int c = U.c_lo; c < U.c_hi; ++c, ++q) {
+      // One chunk.  J >= 0: position J of an NSIG-aligned block of chunks
+      // (q % NSIG == J), so the TMEM buffer, its phase and the sigma slot are
+      // compile-time constants and only the sigma phase (one bit per block)
+      // is a register; J < 0: any position (indices from q).
+      auto chunk_step = [&](auto JC) {
+        constexpr int J = decltype(JC)::value;
+        const uint32_t b = J >= 0 ? (uint32_t)(J & (NB - 1)) : (q & (NB - 1));
+        const uint32_t tp = (q / NB) & 1u;  // (q == block start + J in an aligned block)
+        const uint32_t sl = J >= 0 ? (uint32_t)J : (q & (NSIG - 1));
+        const uint32_t sp = (q / NSIG) & 1u;
         // the chunk's partial: load all of it, then release the TMEM buffer
         if (warp == 0) trace_at(p, q, 3);
-        mbar_wait_a(a_tfull + lbuf * 8, ltph);
+        mbar_wait_a(a_tfull + b * 8, tp);
         if (warp == 0) trace_at(p, q, 4);
-        if (warp == EPIW - 1) trace_at(p, q, 8);
         tc_fence_after();
         float v[COLS];
 #pragma unroll
-        for (int h = 0; h < COLS / 16; ++h) tmem_ld16_nw(t_ld + lbuf * BN + h * 16, v + h * 16);
+        for (int h = 0; h < COLS / 16; ++h) tmem_ld16_nw(t_ld + b * BN + h * 16, v + h * 16);
         tmem_wait_ld();
         reg_fence<COLS>(v);
         tc_fence_before();
         __syncwarp();
-        arrive_e(a_tempty + lbuf * 8);
-        if (pend != NSIG) arrive_e(a_sempty + pend * 8);
+        arrive_e(a_tempty + b * 8);
+        // the previous chunk's sigma slot (released one chunk late, see above)
+        if (J > 0 || q != 0) arrive_e(a_sempty + ((sl - 1) & (NSIG - 1)) * 8);
         if (warp == 0) trace_at(p, q, 5);
-        if (++lbuf == NB) { lbuf = 0; ltph ^= 1; }
         // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
-        mbar_wait_a(a_sfull + slot * 8, sph);
+        mbar_wait_a(a_sfull + sl * 8, sp);
         if (warp == 0) trace_at(p, q, 6);
-        const uint32_t so = slot * SIG_SLOT;
+        const uint32_t so = sl * SIG_SLOT;
         const float sa = ld_shared_f32(sig_a + so);
 #pragma unroll
         for (int i = 0; i < COLS; i += 4) {
@@ -571,11 +578,26 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           fma2(acc[i], acc[i + 1], w0, w1, v[i], v[i + 1]);
           fma2(acc[i + 2], acc[i + 3], w2, w3, v[i + 2], v[i + 3]);
         }
-        pend = slot;
         if (warp == 0) trace_at(p, q, 7);
-        if (warp == EPIW - 1) trace_at(p, q, 9);
-        if (++slot == NSIG) { slot = 0; sph ^= 1; }
+        ++q;
+      };
+      int c = U.c_lo;
+#pragma unroll 1
+      while (c < U.c_hi && (q & (NSIG - 1))) { chunk_step(std::integral_constant<int, -1>{}); ++c; }
+#pragma unroll 1
+      for (; c + NSIG <= U.c_hi; c += NSIG) {
+        static_assert(NSIG == 8, "the aligned block below is written for eight sigma slots");
+        chunk_step(std::integral_constant<int, 0>{});
+        chunk_step(std::integral_constant<int, 1>{});
+        chunk_step(std::integral_constant<int, 2>{});
+        chunk_step(std::integral_constant<int, 3>{});
+        chunk_step(std::integral_constant<int, 4>{});
+        chunk_step(std::integral_constant<int, 5>{});
+        chunk_step(std::integral_constant<int, 6>{});
+        chunk_step(std::integral_constant<int, 7>{});
       }
+#pragma unroll 1
+      for (; c < U.c_hi; ++c) chunk_step(std::integral_constant<int, -1>{});
       // store the tile row (masked to M x N): the output, or this split's f32 partial
       void* const cout = GROUPED ? gt->g[U.g].c : p.c;
       const int n_out = GROUPED ? gt->g[U.g].n : p.N;
@@ -641,9 +663,9 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         }
       }
     }
-    if (pend != NSIG) {  // (the last slot: nothing refills it, released for symmetry)
+    if (q != 0) {  // (the last slot: nothing refills it, released for symmetry)
       __syncwarp();
-      arrive_e(a_sempty + pend * 8);
+      arrive_e(a_sempty + ((q - 1) & (NSIG - 1)) * 8);
     }
   }
 
@@ -1440,6 +1462,12 @@ int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_
     if (tiles_m >= 2) return bf ? mbs::launch2<true, true>(a, b, c, ldc, st) : mbs::launch2<true, false>(a, b, c, ldc, st);
     return bf ? mbs::launch2<false, true>(a, b, c, ldc, st) : mbs::launch2<false, false>(a, b, c, ldc, st);
   }
+  static int bn_dev = -1;
+  if (bn_dev < 0) {
+    const char* e = getenv("MXQ_MBS_BN");  // development A/B of the tile shape
+    bn_dev = e ? atoi(e) : 0;
+  }
+  if (bn_dev == 128) return launch_shape<128, 3, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
   return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
 }
 
