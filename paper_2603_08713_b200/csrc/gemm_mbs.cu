@@ -484,7 +484,9 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
               // scales in a few column groups at the Llama qkv shape when the
               // MMA issue runs a stage ahead), so wait for their commit.
               sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
+#ifndef MXQ_NO_SFFREE
               if (g >= NSFB) mbar_wait_a(a_sffree + (g & (NSFB - 1)) * 8, ((g / NSFB) - 1) & 1u);
+#endif
               mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
               trace_at(p, q, 10);
               tc_fence_after();
@@ -560,9 +562,11 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         reg_fence<COLS>(v);
         tc_fence_before();
         __syncwarp();
-        arrive_e(a_tempty + b * 8);
-        // the previous chunk's sigma slot (released one chunk late, see above)
-        if (J > 0 || q != 0) arrive_e(a_sempty + ((sl - 1) & (NSIG - 1)) * 8);
+        if (lane == 0) {
+          mbar_arrive_a(a_tempty + b * 8);
+          // the previous chunk's sigma slot (released one chunk late, see above)
+          if (J > 0 || q != 0) mbar_arrive_a(a_sempty + ((sl - 1) & (NSIG - 1)) * 8);
+        }
         if (warp == 0) trace_at(p, q, 5);
         // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
         mbar_wait_a(a_sfull + sl * 8, sp);
