@@ -13,8 +13,13 @@ same shapes: plain MXFP4 (OCP32 block-32, kind::mxf4), MX16+OAS and NVFP4.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun): every layer is column-sharded (weight rows) across ranks and
-the bf16 outputs are all-gathered over NVLink (strong scaling, SURVEY §8 e).
+N > 1 (torchrun, default --mode columns): every layer is column-sharded
+(weight rows) across ranks (parallel.column_parallel_forward) and the bf16
+outputs are all-gathered over NVLink into the (M, N) product, the gather of
+row block i overlapped with the GEMM of block i+1 (strong scaling, SURVEY
+section 8 e).  --mode replicas: own tokens per rank, no collective (weak);
+--mode layers: C3, Qwen3-8B weight quantization + prefill with the layers
+sharded; --workload llama70b-ffn: C4's 70B FFN GEMM.
 `--impl reference` times the reference algorithm (the CPU oracle port,
 oracle/mxq_oracle.py) on the host cores on a bounded row sample of the same
 workload; under torchrun only rank 0 runs it.
@@ -110,6 +115,28 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
+# workloads (SURVEY section 8 d; Appendix B shapes)
+# ---------------------------------------------------------------------------
+WORKLOADS = {
+    # C2 (and the N>1 column-sharded form of it): the four Llama-3-8B linears
+    "llama8b": LAYERS,
+    # C4: the Llama-3-70B FFN gate/up GEMM, K = 8192, N = 28672
+    "llama70b-ffn": (("ffn_gate_up", 28672, 8192),),
+}
+# C3: Qwen3-8B, 36 layers x 7 projections (name, N, K)
+QWEN3_8B = (("q", 4096, 4096), ("k", 1024, 4096), ("v", 1024, 4096), ("o", 4096, 4096),
+            ("gate", 12288, 4096), ("up", 12288, 4096), ("down", 4096, 12288))
+QWEN3_LAYERS = 36
+
+
+def synth_activation(torch, dev, rows, k, gen):
+    """N(0, 1) with 1% x100 outliers (config 1's generator), bf16."""
+    x = torch.randn(rows, k, device=dev, generator=gen)
+    hit = torch.rand(rows, k, device=dev, generator=gen) < 0.01
+    return torch.where(hit, x * 100.0, x).to(torch.bfloat16)
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours(args):
@@ -133,58 +160,14 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    mode = args.mode
+    if mode == "auto":
+        mode = "columns" if world > 1 else "single"
+    if mode == "layers":
+        return run_layers(args, world, rank, local, dev, backend)
+    layers = WORKLOADS[args.workload]
     V = M.Variant
     bf16 = torch.bfloat16
-
-    # ---- synthetic inputs (activations replicated, weights sharded) --------
-    g = torch.Generator(device=dev).manual_seed(1234)
-    acts = []
-    for _, n, k in LAYERS:
-        x = torch.randn(M_TOK, k, device=dev, generator=g)
-        hit = torch.rand(M_TOK, k, device=dev, generator=g) < 0.01
-        acts.append(torch.where(hit, x * 100.0, x).to(bf16))
-    gw = torch.Generator(device=dev).manual_seed(4321 + rank)
-    wdense, bounds = [], []
-    cols = args.mode == "columns" and world > 1  # tensor-parallel column shards + all_gather
-    for _, n, k in LAYERS:
-        lo, hi = P.shard_bounds(n, world, rank) if cols else (0, n)
-        bounds.append((lo, hi))
-        wdense.append((torch.randn(hi - lo, k, device=dev, generator=gw) * 0.02).to(bf16))
-
-    arms = {  # name -> (activation variant, weight variant)
-        "mbs_h": (V.MBS_S, V.MBS_D),
-        "ocp32": (V.OCP32, V.OCP32),
-        "mx16_oas": (V.MX16_OAS, V.MX16_OAS),
-        "nvfp4": (V.NVFP4, V.NVFP4),
-    }
-    weights = {name: [M.quantize_tensor(w, M.SchemeConfig(wv)) for w in wdense] for name, (_, wv) in arms.items()}
-    del wdense
-    outs = [torch.empty(M_TOK, hi - lo, device=dev, dtype=bf16) for lo, hi in bounds]
-    gathered = [torch.empty(world * M_TOK, max(P.shard_bounds(n, world, r)[1] - P.shard_bounds(n, world, r)[0]
-                                               for r in range(world)), device=dev, dtype=bf16)
-                if cols else None for _, n, _ in LAYERS]
-    n_local_frac = sum(2.0 * M_TOK * (hi - lo) * k for (lo, hi), (_, _, k) in zip(bounds, LAYERS))
-    # replicas (default): every rank runs the whole step on its own M tokens,
-    # no data-path collective, weak scaling; columns: one step split by output
-    # column across ranks plus the bf16 all_gather (config 4's pattern)
-    step_flops_global = flops_per_step() * (1 if cols else world)
-
-    def step(arm, gemm_events=None):
-        av, _ = arms[arm]
-        for li in range(len(LAYERS)):
-            aq = M.quantize_tensor(acts[li], M.SchemeConfig(av), check=False)
-            if gemm_events is not None:
-                gemm_events[li][0].record()
-            M.matmul_quantized(aq, weights[arm][li], out=outs[li], out_dtype=bf16, check=False)
-            if gemm_events is not None:
-                gemm_events[li][1].record()
-            if cols:
-                send = outs[li]
-                if send.shape[1] != gathered[li].shape[1]:
-                    pad = torch.zeros(M_TOK, gathered[li].shape[1], device=dev, dtype=bf16)
-                    pad[:, : send.shape[1]] = send
-                    send = pad
-                dist.all_gather_into_tensor(gathered[li], send)
 
     def barrier():
         if world > 1:
@@ -194,94 +177,245 @@ def run_ours(args):
                 dist.barrier()
         torch.cuda.synchronize()
 
-    graphs = {}
+    # ---- synthetic inputs: activations replicated (same seed on every rank
+    # in columns mode, own tokens per rank in replicas mode); weights random
+    # init N(0, 0.02), row-sharded in columns mode -----------------------------
+    cols = mode == "columns" and world > 1
+    g = torch.Generator(device=dev).manual_seed(1234 + (rank if mode == "replicas" else 0))
+    acts = [synth_activation(torch, dev, M_TOK, k, g) for _, n, k in layers]
+    gw = torch.Generator(device=dev).manual_seed(4321)
+    wdense, bounds = [], []
+    for _, n, k in layers:
+        full = (torch.randn(n, k, device=dev, generator=gw) * 0.02).to(bf16)
+        lo, hi = P.shard_bounds(n, world, rank) if cols else (0, n)
+        bounds.append((lo, hi))
+        wdense.append(full[lo:hi].contiguous())
+        del full
 
-    def capture(arm):
-        """The whole step (4 x quantize + GEMM [+ all_gather]) as one CUDA graph."""
-        if cols:
-            return None  # NCCL collectives are replayed eagerly
+    arms = {  # name -> (activation variant, weight variant)
+        "mbs_h": (V.MBS_S, V.MBS_D),
+        "ocp32": (V.OCP32, V.OCP32),
+        "mx16_oas": (V.MX16_OAS, V.MX16_OAS),
+        "nvfp4": (V.NVFP4, V.NVFP4),
+    }
+    weights = {name: [M.quantize_tensor(w, M.SchemeConfig(wv)) for w in wdense] for name, (_, wv) in arms.items()}
+    del wdense
+    outs = [torch.empty(M_TOK, hi - lo, device=dev, dtype=bf16) for lo, hi in bounds]   # local products
+    full_outs = [torch.empty(M_TOK, n, device=dev, dtype=bf16) for _, n, _ in layers] if cols else None
+    n_local = sum(2.0 * M_TOK * (hi - lo) * k for (lo, hi), (_, _, k) in zip(bounds, layers))
+    step_flops_global = sum(2.0 * M_TOK * n * k for _, n, k in layers) * (1 if cols else world)
+    comm = torch.cuda.Stream() if cols else None
+
+    def local_step(arm, li, x, dst):
+        av, _ = arms[arm]
+        aq = M.quantize_tensor(x, M.SchemeConfig(av), check=False)
+        M.matmul_quantized(aq, weights[arm][li], out=dst, out_dtype=bf16, check=False)
+
+    def step(arm):
+        for li in range(len(layers)):
+            if cols:
+                # column shards + overlapped all_gather into the (M, N) product
+                P.column_parallel_forward(acts[li], weights[arm][li], full_outs[li], world,
+                                          lambda x, wq, dst, li=li: local_step(arm, li, x, dst),
+                                          chunks=args.chunks, comm_stream=comm)
+            else:
+                local_step(arm, li, acts[li], outs[li])
+
+    def gemm_only(arm, aqs):
+        for li in range(len(layers)):
+            M.matmul_quantized(aqs[li], weights[arm][li], out=outs[li], out_dtype=bf16, check=False)
+
+    def capture(fn):
+        """fn() as one CUDA graph (warmed once on a side stream)."""
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
-            step(arm)  # warm (allocations, attributes, descriptors)
+            fn()
         torch.cuda.current_stream().wait_stream(s)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            step(arm)
-        return g
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        return gr
 
-    def run_step(arm):
-        g = graphs.get(arm)
-        if g is not None:
-            g.replay()
-        else:
-            step(arm)
-
-    def time_steps(arm, k, w):
-        if args.graphs and arm not in graphs:
-            graphs[arm] = capture(arm)
+    def timed(fn, k, w):
         for _ in range(w):
-            run_step(arm)
+            fn()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(k):
-            run_step(arm)
+            fn()
         e1.record()
         barrier()
-        ms = e0.elapsed_time(e1) / k
-        return P.max_over_ranks(ms, device=dev)
-
-    def time_gemms(arm, k):
-        """Per-launch device time of the dominant kernel (the GEMM)."""
-        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in LAYERS] for _ in range(k)]
-        barrier()
-        for i in range(k):
-            step(arm, evs[i])
-        barrier()
-        per_layer = [float(np.mean([evs[i][li][0].elapsed_time(evs[i][li][1]) for i in range(k)]))
-                     for li in range(len(LAYERS))]
-        return per_layer
+        return P.max_over_ranks(e0.elapsed_time(e1) / k, device=dev)
 
     K, W = args.steps, args.warmup
     results = {}
     with Clocks(local) as clocks:
         for arm in ("mbs_h", "ocp32", "mx16_oas", "nvfp4"):
-            ms = time_steps(arm, K, W)
-            gl = time_gemms(arm, max(3, K // 2))
-            gemm_ms = sum(gl)
+            if args.graphs and not cols:
+                gs = capture(lambda: step(arm))
+                ms = timed(gs.replay, K, W)
+            else:  # NCCL collectives and the comm stream run eagerly
+                ms = timed(lambda: step(arm), K, W)
+            # the dominant kernel alone: the step's GEMM launches (operands
+            # quantized beforehand) replayed as one graph, device time per step
+            aqs = [M.quantize_tensor(a, M.SchemeConfig(arms[arm][0]), check=False) for a in acts]
+            if args.graphs:
+                gg = capture(lambda: gemm_only(arm, aqs))
+                gemm_ms = timed(gg.replay, K, W)
+            else:
+                gemm_ms = timed(lambda: gemm_only(arm, aqs), K, W)
             results[arm] = {
                 "ms_per_step": ms,
                 "tflops_step": step_flops_global / (ms * 1e-3) / 1e12,
                 "gemm_ms": gemm_ms,
-                "gemm_tflops": n_local_frac / (gemm_ms * 1e-3) / 1e12 * world,  # all ranks' GEMM work / per-rank time
-                "gemm_ms_per_layer": {name: t for (name, _, _), t in zip(LAYERS, gl)},
+                "gemm_tflops": n_local * world / (gemm_ms * 1e-3) / 1e12,  # all ranks' GEMM work / max per-rank time
             }
+            del aqs
     head = results["mbs_h"]
 
     # ---- quantizer bandwidth (4096x4096 bf16 activations, HBM-cold) -------
     # the timed launches cycle over 8 distinct activations (256 MB, twice the
     # L2), so every launch streams its input from HBM
-    qbw = {}
+    qbw = quantizer_bandwidth(torch, M, dev, args)
+
+    out = None
+    if rank == 0:
+        out = {}
+        # ---- QSNR on config 1 (4096x4096 gaussian+outliers seed 0, bf16) ----
+        t1 = M.generate_tensor(M.GeneratorSpec("gaussian_with_outliers", (4096, 4096), seed=0))
+        t1b = torch.from_numpy(t1).to(dev).to(bf16)
+        meta = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_meta.json")))
+        qs = {}
+        for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4"):
+            q = M.quantize_tensor(t1b, M.SchemeConfig(V(vname)))
+            rep, fl = M.qsnr_quantized(t1b, q)
+            ref = meta["config1"][vname]
+            qs[vname] = {"qsnr_db": round(rep.qsnr_db, 6), "flush": round(fl, 6),
+                         "equals_reference": rep.qsnr_db == ref["qsnr_db"] and fl == ref["flush"]}
+        out["qsnr"] = qs
+
+    # ---- e2e: public API, pinned host activations in, bf16 products out ----
+    e2e = run_e2e(torch, M, P, dev, world, args, acts, outs, weights["mbs_h"], step_flops_global, barrier,
+                  len(layers), cols)
+    if world > 1:
+        barrier()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (tcgen05 MBS GEMM) -----------------
+    clk = clocks.summary()
+    roofline = gemm_roofline(head["gemm_tflops"] / world, clk)
+
+    # ---- CPU baseline: the reference algorithm (oracle port) on a sample ---
+    cpu = cpu_baseline_sample(weights_from_gpu=[weights["mbs_h"][li] for li in range(len(layers))],
+                              acts=acts, rows=args.cpu_rows) if (world == 1 and args.workload == "llama8b") else None
+
+    ocp = results["ocp32"]
+    par = {"single": "single", "replicas": f"replicas x{world} (own tokens per rank, no collective)",
+           "columns": f"column-shard x{world} (weight rows) + overlapped NCCL all_gather of the bf16 outputs "
+                      f"into (M, N), {args.chunks} row blocks"}[mode if world > 1 else "single"]
+    wl_desc = WORKLOAD if args.workload == "llama8b" else (
+        "llama3-70b FFN gate/up N=28672 K=8192; M=4096 tokens; A quantized per step (MBS_S) x resident W (MBS_D); bf16 out")
+    line = {
+        "metric": METRIC, "value": round(head["tflops_step"], 2), "unit": "TFLOP/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
+        "scaling": "strong" if cols else "weak", "vs_baseline": None,
+        "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
+        "data": "synthetic (activations N(0,1) with 1% x100 outliers; random-init N(0,0.02) weights)",
+        "config": {"workload": wl_desc, "global_batch": M_TOK * (1 if cols else world), "seq_len": None,
+                   "parallelism": par,
+                   "l2": "inputs larger than L2 (218 MB bf16 activations + 121 MB fp4 weights per step)"},
+        "gemm_only_tflops": round(head["gemm_tflops"], 2),
+        "arms": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                 for k, v in results.items()},
+        "mbs_h_overhead_vs_ocp32": round(1.0 - head["tflops_step"] / ocp["tflops_step"], 4),
+        "mbs_h_gemm_overhead_vs_ocp32": round(1.0 - head["gemm_tflops"] / ocp["gemm_tflops"], 4),
+        "mbs_h_overhead_vs_nvfp4": round(1.0 - head["tflops_step"] / results["nvfp4"]["tflops_step"], 4),
+        "quantizer": {k: {kk: round(vv, 2) for kk, vv in v.items()} for k, v in qbw.items()},
+        "quantizer_hbm_frac_mbs_s": round(qbw["mbs_s"]["gbs"] / hbm_peak(), 4),
+        "qsnr_config1": out["qsnr"],
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 8 * K,
+        "clocks": clk,
+    }
+    if cols:
+        line["gather_overhead"] = round(1.0 - head["gemm_ms"] / head["ms_per_step"], 4)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6550.0
+
+
+def gemm_roofline(achieved_per_gpu, clk):
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    bf16_peak = peaks.get("bf16_tflops")
+    basis = "4 x measured dense bf16 (MEASURED_PEAKS.json bf16_tflops, burst): FP4 dense = 4x bf16 on B200"
+    if not bf16_peak:
+        bf16_peak, basis = 1590.0, "4 x fallback dense bf16 1.59 PF (B200_PROFILING.md)"
+    fp4_peak = 4.0 * bf16_peak
+    traffic, tbasis = None, "no ncu capture committed"
+    prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(prof):
+        try:
+            tj = json.load(open(prof))
+            traffic, tbasis = tj.get("mbs_h_bytes_per_launch"), tj.get("basis", tbasis)
+        except Exception:
+            pass
+    # MBS-specific ceiling (DESIGN.md section 3): the epilogue folds every
+    # 128-K macro partial with two FP32 ops per output, 128 FP32 lanes/clk/SM
+    # -> 64 output-macros x 128 K x 2 flop per clock per SM
+    f_mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
+    fp32_bound = 148 * 64 * 128 * 2 * f_mhz * 1e6 / 1e12
+    return {"bound": "tensor", "achieved": round(achieved_per_gpu, 1), "peak": round(fp4_peak, 1), "unit": "TFLOP/s",
+            "frac": round(achieved_per_gpu / fp4_peak, 4), "traffic": traffic, "peak_basis": basis,
+            "kernel": "mbs::k_gemm_mbs<BN=192,NB=2,bf16,CL=2> (kind::mxf4nvf4.block16 UE8M0, N=192 MMAs, "
+                      "tcgen05.cp scale factors, 16 FP32 epilogue warps)",
+            "mbs_fp32_epilogue_bound": round(fp32_bound, 1),
+            "frac_of_mbs_fp32_bound": round(achieved_per_gpu / fp32_bound, 4),
+            "mbs_bound_basis": f"2 FP32 ops per output per 128-K macro at 128 FP32 lanes/clk/SM, {f_mhz:.0f} MHz",
+            "traffic_basis": tbasis,
+            "algorithmic": "2*M*N*K summed over the step's GEMM launches / device time of a CUDA graph holding "
+                           "exactly those launches (operands quantized beforehand), CUDA events on the launch stream"}
+
+
+def quantizer_bandwidth(torch, M, dev, args):
+    V = M.Variant
     gq = torch.Generator(device=dev).manual_seed(1234)
-    xq = [torch.randn(M_TOK, 4096, device=dev, generator=gq).to(bf16) for _ in range(8)]
+    xq = [torch.randn(M_TOK, 4096, device=dev, generator=gq).to(torch.bfloat16) for _ in range(8)]
     # algorithmic bytes / element: bf16 read + packed codes + scale bytes
     # (+ MBS mantissa byte per 128 elements); the GEMM-layout copies the
     # kernels also write (row-major + MMA-atom scales, f32 sigma) are not
     # counted, so the GB/s is conservative.
     bytes_per_el = {"ocp32": 2 + 0.5 + 1 / 32, "mx16": 2 + 0.5 + 1 / 16, "mx16_oas": 2 + 0.5 + 1 / 16,
                     "mbs_s": 2 + 0.5 + 1 / 16 + 1 / 128, "mbs_d": 2 + 0.5 + 1 / 16 + 1 / 128,
-                    "nvfp4": 2 + 0.5 + 1 / 16}
-    for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "nvfp4", "mbs_d"):
-        cfg = M.SchemeConfig(V(vname))
-        reps = 8 if vname == "mbs_d" else 48
+                    "nvfp4": 2 + 0.5 + 1 / 16, "mbs_d_lut": 2 + 0.5 + 1 / 16 + 1 / 128}
+    qbw = {}
+    for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "nvfp4", "mbs_d", "mbs_d_lut"):
+        cfg = M.SchemeConfig(V.MBS_D, mbs_mode="lut") if vname == "mbs_d_lut" else M.SchemeConfig(V(vname))
+        reps = 8 if vname.startswith("mbs_d") else 48
         for x in xq:
             M.quantize_tensor(x, cfg, check=False, gemm_layout=True)
         torch.cuda.synchronize()
         g = None
-        if args.graphs and vname != "mbs_d":  # MBS-D uploads its candidate table per call
+        if args.graphs:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 for i in range(reps):
@@ -301,173 +435,178 @@ def run_ours(args):
         qbw[vname] = {"us": ms * 1e3, "gbs": xq[0].numel() * bytes_per_el[vname] / (ms * 1e-3) / 1e9,
                       "melem_s": xq[0].numel() / (ms * 1e-3) / 1e6}
     del xq
+    return qbw
 
-    out = None
-    if rank == 0:
-        out = {}
-        # ---- QSNR on config 1 (4096x4096 gaussian+outliers seed 0, bf16) ----
-        t1 = M.generate_tensor(M.GeneratorSpec("gaussian_with_outliers", (4096, 4096), seed=0))
-        t1b = torch.from_numpy(t1).to(dev).to(bf16)
-        meta = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_meta.json")))
-        qs = {}
-        for vname in ("ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4"):
-            q = M.quantize_tensor(t1b, M.SchemeConfig(V(vname)))
-            rep, fl = M.qsnr_quantized(t1b, q)
-            ref = meta["config1"][vname]
-            qs[vname] = {"qsnr_db": round(rep.qsnr_db, 6), "flush": round(fl, 6),
-                         "equals_reference": rep.qsnr_db == ref["qsnr_db"] and fl == ref["flush"]}
-        out["qsnr"] = qs
 
-    # ---- e2e: public API, pinned host activations in, bf16 out -------------
-    # every rank (replicas) runs its own step from its own pinned host buffers;
-    # the time is the max over ranks
-    e2e = None
-    if not cols:
-        host_in = [a.cpu().pin_memory() for a in acts]
-        host_out = [torch.empty(o.shape, dtype=bf16).pin_memory() for o in outs]
-        # two device buffer sets: step i+1's uploads and GEMMs run while step
-        # i's products are still being read back (steps pipelined as a server
-        # would run them; every step still moves all its bytes)
-        dev_in = [[torch.empty_like(a) for a in acts] for _ in range(2)]
-        dev_out = [[torch.empty_like(o) for o in outs] for _ in range(2)]
-        cfg_a = M.SchemeConfig(V.MBS_S)
-        s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
-        comp = torch.cuda.current_stream()
-        consumed = [[None] * len(LAYERS) for _ in range(2)]   # compute done reading dev_in[b][li]
-        drained = [[None] * len(LAYERS) for _ in range(2)]    # D2H done reading dev_out[b][li]
-        statuses = []
+def run_e2e(torch, M, P, dev, world, args, acts, outs, wq, step_flops_global, barrier, n_layers, cols):
+    """The headline step through the public API from pinned HOST bf16
+    activations to HOST bf16 products.  Every rank uploads the (replicated or
+    own) activations and downloads its own products (columns mode: its column
+    shard -- the host holds the whole product across ranks); the time is the
+    max over ranks."""
+    bf16 = torch.bfloat16
+    V = M.Variant
+    host_in = [a.cpu().pin_memory() for a in acts]
+    host_out = [torch.empty(o.shape, dtype=bf16).pin_memory() for o in outs]
+    # two device buffer sets: step i+1's uploads and GEMMs run while step i's
+    # products are still being read back (steps pipelined as a server would
+    # run them; every step still moves all its bytes)
+    dev_in = [[torch.empty_like(a) for a in acts] for _ in range(2)]
+    dev_out = [[torch.empty_like(o) for o in outs] for _ in range(2)]
+    cfg_a = M.SchemeConfig(V.MBS_S)
+    s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    comp = torch.cuda.current_stream()
+    consumed = [[None] * n_layers for _ in range(2)]   # compute done reading dev_in[b][li]
+    drained = [[None] * n_layers for _ in range(2)]    # D2H done reading dev_out[b][li]
+    statuses = []
 
-        def e2e_step(it):
-            # H2D on one copy engine, D2H on the other, compute in between:
-            # layer li's input lands while li-1 computes, its product leaves
-            # while li+1 computes (PCIe is full duplex)
-            b = it % 2
-            landed = []
-            for li in range(len(LAYERS)):
-                with torch.cuda.stream(s_h2d):
-                    if consumed[b][li] is not None:
-                        s_h2d.wait_event(consumed[b][li])
-                    dev_in[b][li].copy_(host_in[li], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(s_h2d)
-                landed.append(ev)
-            for li in range(len(LAYERS)):
-                comp.wait_event(landed[li])
-                if drained[b][li] is not None:
-                    comp.wait_event(drained[b][li])
-                # public API; the non-finite status is checked after the timed region
-                aq = M.quantize_tensor(dev_in[b][li], cfg_a, check=False)
-                statuses.append(aq._cache["status"])
-                M.matmul_quantized(aq, weights["mbs_h"][li], out=dev_out[b][li], out_dtype=bf16, check=False)
-                done = torch.cuda.Event()
-                done.record(comp)
-                consumed[b][li] = done
-                with torch.cuda.stream(s_d2h):
-                    s_d2h.wait_event(done)
-                    host_out[li].copy_(dev_out[b][li], non_blocking=True)
-                    dr = torch.cuda.Event()
-                    dr.record(s_d2h)
-                    drained[b][li] = dr
+    def e2e_step(it):
+        # H2D on one copy engine, D2H on the other, compute in between: layer
+        # li's input lands while li-1 computes, its product leaves while li+1
+        # computes (PCIe is full duplex)
+        b = it % 2
+        landed = []
+        for li in range(n_layers):
+            with torch.cuda.stream(s_h2d):
+                if consumed[b][li] is not None:
+                    s_h2d.wait_event(consumed[b][li])
+                dev_in[b][li].copy_(host_in[li], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(s_h2d)
+            landed.append(ev)
+        for li in range(n_layers):
+            comp.wait_event(landed[li])
+            if drained[b][li] is not None:
+                comp.wait_event(drained[b][li])
+            # public API; the non-finite status is checked after the timed region
+            aq = M.quantize_tensor(dev_in[b][li], cfg_a, check=False)
+            statuses.append(aq._cache["status"])
+            M.matmul_quantized(aq, wq[li], out=dev_out[b][li], out_dtype=bf16, check=False)
+            done = torch.cuda.Event()
+            done.record(comp)
+            consumed[b][li] = done
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(done)
+                host_out[li].copy_(dev_out[b][li], non_blocking=True)
+                dr = torch.cuda.Event()
+                dr.record(s_d2h)
+                drained[b][li] = dr
 
-        for it in range(max(2, W // 2)):
-            e2e_step(it)
-        torch.cuda.synchronize()
-        ke = max(4, K // 2)
-        barrier()
-        t0 = time.perf_counter()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for it in range(ke):
-            e2e_step(it)
-        comp.wait_stream(s_d2h)   # the last step's products are on the host
-        e1.record()
-        torch.cuda.synchronize()
-        ms_e2e = P.max_over_ranks(e0.elapsed_time(e1) / ke, device=dev)
-        wall = P.max_over_ranks((time.perf_counter() - t0) * 1e3 / ke, device=dev)
-        for st in statuses:
-            M._lib.raise_on_status(st)
-        host_ok = bool(torch.equal(host_out[0], dev_out[(ke - 1) % 2][0].cpu()))
-        e2e = {"value": step_flops_global / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
-               "h2d_bytes_per_step": int(sum(a.numel() * 2 for a in acts)) * world,
-               "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)) * world,
-               "ms_per_step": ms_e2e, "wall_ms_per_step": wall, "steps": ke,
-               "pipelined": "step i+1's uploads and GEMMs overlap step i's downloads (double-buffered); "
-                            "the timed region ends when the last step's products are in host memory",
-               "host_copy_matches_device": host_ok}
-    if world > 1:
-        barrier()
+    W, K = args.warmup, args.steps
+    for it in range(max(2, W // 2)):
+        e2e_step(it)
+    torch.cuda.synchronize()
+    ke = max(4, K // 2)
+    barrier()
+    t0 = time.perf_counter()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for it in range(ke):
+        e2e_step(it)
+    comp.wait_stream(s_d2h)   # the last step's products are on the host
+    e1.record()
+    torch.cuda.synchronize()
+    ms_e2e = P.max_over_ranks(e0.elapsed_time(e1) / ke, device=dev)
+    wall = P.max_over_ranks((time.perf_counter() - t0) * 1e3 / ke, device=dev)
+    for st in statuses:
+        M._lib.raise_on_status(st)
+    host_ok = bool(torch.equal(host_out[0], dev_out[(ke - 1) % 2][0].cpu()))
+    return {"value": step_flops_global / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": int(sum(a.numel() * 2 for a in acts)) * world,
+            "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)) * world,
+            "ms_per_step": ms_e2e, "wall_ms_per_step": wall, "steps": ke,
+            "pipelined": "step i+1's uploads and GEMMs overlap step i's downloads (double-buffered); "
+                         "the timed region ends when the last step's products are in host memory",
+            "host_copy_matches_device": host_ok}
 
-    if rank != 0:
+
+def run_layers(args, world, rank, local, dev, backend):
+    """C3: Qwen3-8B whole-model weight quantization (MBS-D exact) + prefill
+    GEMMs (MBS-H, M = 4096), the 36 layers sharded over the ranks
+    (parallel.layer_owner); no exchange.  A step = quantize every owned
+    layer's 7 weight matrices from bf16 + run their prefill GEMMs (activation
+    quantization included).  value = all ranks' prefill GEMM FLOPs / the
+    max-over-ranks step time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_08713_b200 as M
+    from paper_2603_08713_b200 import parallel as P
+
+    V = M.Variant
+    bf16 = torch.bfloat16
+    owner = P.layer_owner(QWEN3_LAYERS, world)
+    mine = [l for l in range(QWEN3_LAYERS) if owner[l] == rank]
+    # weights of the owned layers, seeded per (layer, projection)
+    wdense = {}
+    for l in mine:
+        for pi, (name, n, k) in enumerate(QWEN3_8B):
+            gw = torch.Generator(device=dev).manual_seed(10_000 * l + pi)
+            wdense[(l, pi)] = (torch.randn(n, k, device=dev, generator=gw) * 0.02).to(bf16)
+    g = torch.Generator(device=dev).manual_seed(99)
+    acts = {k: synth_activation(torch, dev, M_TOK, k, g) for k in sorted({k for _, _, k in QWEN3_8B})}
+    outs = {pi: torch.empty(M_TOK, n, device=dev, dtype=bf16) for pi, (_, n, _) in enumerate(QWEN3_8B)}
+    wcfg, acfg = M.SchemeConfig(V.MBS_D), M.SchemeConfig(V.MBS_S)
+
+    def quantize_weights():
+        return {key: M.quantize_tensor(w, wcfg, check=False) for key, w in wdense.items()}
+
+    def prefill(wq):
+        for (l, pi), q in wq.items():
+            _, n, k = QWEN3_8B[pi]
+            aq = M.quantize_tensor(acts[k], acfg, check=False)
+            M.matmul_quantized(aq, q, out=outs[pi], out_dtype=bf16, check=False)
+
+    def barrier():
         if world > 1:
-            dist.destroy_process_group()
-        return
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
+        torch.cuda.synchronize()
 
-    # ---- roofline of the dominant kernel (tcgen05 GEMM, MBS-H) -------------
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        pass
-    bf16_peak = peaks.get("bf16_tflops")
-    basis = "4 x measured dense bf16 (MEASURED_PEAKS.json bf16_tflops, burst): FP4 dense = 4x bf16 on B200"
-    if not bf16_peak:
-        bf16_peak, basis = 1590.0, "4 x fallback dense bf16 1.59 PF (B200_PROFILING.md)"
-    fp4_peak = 4.0 * bf16_peak
-    achieved = head["gemm_tflops"]
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("mbs_h_bytes_per_launch")
-        except Exception:
-            traffic = None
-    # MBS-specific ceiling: the epilogue folds every
-    # 128-K macro partial with two FP32 ops per output, 128 FP32 lanes/clk/SM
-    # -> 64 output-macros x 128 K x 2 flop per clock per SM
-    clk = clocks.summary()
-    f_mhz = clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0
-    fp32_bound = 148 * 64 * 128 * 2 * f_mhz * 1e6 / 1e12
-    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(fp4_peak, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / fp4_peak, 4), "traffic": traffic, "peak_basis": basis,
-                "kernel": "mbs::k_gemm_mbs<BN=192,NB=2,bf16,CL=2> (kind::mxf4nvf4.block16 UE8M0, N=192 MMAs, "
-                          "tcgen05.cp scale factors, 16 FP32 epilogue warps)",
-                "mbs_fp32_epilogue_bound": round(fp32_bound, 1),
-                "frac_of_mbs_fp32_bound": round(achieved / fp32_bound, 4),
-                "mbs_bound_basis": f"2 FP32 ops per output per 128-K macro at 128 FP32 lanes/clk/SM, {f_mhz:.0f} MHz",
-                "traffic_basis": "profiles/gemm_traffic.json: ncu --set full DRAM bytes per launch, mean of the same 4 layer launches",
-                "algorithmic": "2*M*N*K per launch over the 4 layer launches, CUDA events on the launch stream"}
-
-    # ---- CPU baseline: the reference algorithm (oracle port) on a sample ---
-    cpu = cpu_baseline_sample(weights_from_gpu=[weights["mbs_h"][li] for li in range(len(LAYERS))],
-                              acts=acts, rows=args.cpu_rows)
-
-    ocp = results["ocp32"]
-    line = {
-        "metric": METRIC, "value": round(head["tflops_step"], 2), "unit": "TFLOP/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
-        "scaling": "strong" if cols else "weak", "vs_baseline": None,
-        "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
-        "data": "synthetic (activations N(0,1) with 1% x100 outliers; random-init N(0,0.02) weights)",
-        "config": {"workload": WORKLOAD, "global_batch": M_TOK * (1 if cols else world), "seq_len": None,
-                   "parallelism": (f"column-shard x{world} + all_gather" if cols else
-                                   f"replicas x{world} (token-parallel, no collective)") if world > 1 else "single",
-                   "l2": "inputs larger than L2 (218 MB bf16 activations + 121 MB fp4 weights per step)"},
-        "gemm_only_tflops": round(head["gemm_tflops"], 2),
-        "arms": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
-                 for k, v in results.items()},
-        "mbs_h_overhead_vs_ocp32": round(1.0 - head["tflops_step"] / ocp["tflops_step"], 4),
-        "mbs_h_gemm_overhead_vs_ocp32": round(1.0 - head["gemm_tflops"] / ocp["gemm_tflops"], 4),
-        "mbs_h_overhead_vs_nvfp4": round(1.0 - head["tflops_step"] / results["nvfp4"]["tflops_step"], 4),
-        "quantizer": {k: {kk: round(vv, 2) for kk, vv in v.items()} for k, v in qbw.items()},
-        "quantizer_hbm_frac_mbs_s": round(qbw["mbs_s"]["gbs"] / peaks.get("hbm_gbs", 6650.0), 4),
-        "qsnr_config1": out["qsnr"],
-        "roofline": roofline,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": 8 * K,
-        "clocks": clk,
-    }
-    print(json.dumps(line), flush=True)
+    for _ in range(args.warmup):
+        prefill(quantize_weights())
+    barrier()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tq = tp = 0.0
+    with Clocks(local) as clocks:
+        for _ in range(args.steps):
+            e[0].record()
+            wq = quantize_weights()
+            e[1].record()
+            prefill(wq)
+            e[2].record()
+            torch.cuda.synchronize()
+            tq += e[0].elapsed_time(e[1])
+            tp += e[1].elapsed_time(e[2])
+    barrier()
+    tq, tp = tq / args.steps, tp / args.steps
+    t_step = P.max_over_ranks(tq + tp, device=dev)
+    tq_max, tp_max = P.max_over_ranks(tq, device=dev), P.max_over_ranks(tp, device=dev)
+    params = sum(n * k for _, n, k in QWEN3_8B) * QWEN3_LAYERS
+    flops = 2.0 * M_TOK * params
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(flops / (t_step * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
+            "data": "synthetic (random-init N(0,0.02) bf16 weights per (layer, projection); activations "
+                    "N(0,1) with 1% x100 outliers)",
+            "config": {"workload": "qwen3-8b: 36 layers x {q,k,v,o,gate,up,down} (6.95 B params) MBS-D exact "
+                                   "weight quantization + MBS-H prefill GEMMs at M=4096, per step",
+                       "global_batch": M_TOK, "seq_len": None,
+                       "parallelism": f"layer-shard x{world} (parallel.layer_owner, no collective)"},
+            "weight_quant_ms": round(tq_max, 3),
+            "weight_quant_gelem_s": round(params / world / (tq_max * 1e-3) / 1e9, 2),
+            "prefill_ms": round(tp_max, 3),
+            "prefill_tflops": round(flops / (tp_max * 1e-3) / 1e12, 2),
+            "layers_per_rank": len(mine),
+            "gpu_launches": args.steps * len(wdense) * 3,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
@@ -565,8 +704,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--mode", default="replicas", choices=("replicas", "columns"),
-                    help="N>1: independent replicas on their own tokens (weak) or column shards + all_gather (strong)")
+    ap.add_argument("--mode", default="auto", choices=("auto", "replicas", "columns", "layers"),
+                    help="auto: N=1 single GPU, N>1 columns (column shards + overlapped all_gather, strong); "
+                         "replicas: every rank its own tokens (weak, no collective); layers: C3 Qwen3-8B "
+                         "whole-model weight quantization + prefill, layers sharded")
+    ap.add_argument("--workload", default="llama8b", choices=tuple(WORKLOADS),
+                    help="llama8b: the four Llama-3-8B linears (C2); llama70b-ffn: the 70B FFN gate/up (C4)")
+    ap.add_argument("--chunks", type=int, default=4, help="columns mode: row blocks of the gather overlap")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-wrows", type=int, default=2048)

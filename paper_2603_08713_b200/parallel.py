@@ -64,6 +64,66 @@ def gather_columns(local: torch.Tensor, n_total: int, world: int, group=None) ->
     return torch.cat([buf[r, :, : sizes[r]] for r in range(world)], dim=1)
 
 
+def gather_columns_into(local: torch.Tensor, out: torch.Tensor, world: int, staging: torch.Tensor = None,
+                        group=None) -> torch.Tensor:
+    """All-gather every rank's column shard ``local`` (m, n_r) into ``out``
+    (m, N), the row-major product: one ``all_gather_into_tensor`` into a
+    (world, m, width) staging buffer (shards padded to the widest), then one
+    strided copy per rank into its column slice.  ``staging`` may be passed to
+    reuse a buffer across calls."""
+    m, n_total = out.shape
+    spans = [shard_bounds(n_total, world, r) for r in range(world)]
+    width = max(hi - lo for lo, hi in spans)
+    send = local
+    if local.shape[1] != width:
+        send = torch.zeros((m, width), dtype=local.dtype, device=local.device)
+        send[:, : local.shape[1]] = local
+    if staging is None or staging.shape != (world, m, width):
+        staging = torch.empty((world, m, width), dtype=local.dtype, device=local.device)
+    dist.all_gather_into_tensor(staging.view(world * m, width), send.contiguous(), group=group)
+    for r, (lo, hi) in enumerate(spans):
+        out[:, lo:hi].copy_(staging[r, :, : hi - lo])
+    return out
+
+
+def column_parallel_forward(x: torch.Tensor, w_shard, out: torch.Tensor, world: int, local_gemm: Callable,
+                            chunks: int = 4, comm_stream=None, group=None) -> torch.Tensor:
+    """y = x @ W^T into ``out`` (M, N) with W row-sharded across ranks, the
+    gather overlapped with compute.  x is cut into ``chunks`` row blocks;
+    ``local_gemm(x_rows, w_shard, dst)`` writes the block's (rows, n_r) column
+    shard into ``dst``.  Block i+1's GEMM runs on the current stream while
+    block i's all_gather + (M, N) assembly run on ``comm_stream`` (CUDA; on
+    CPU the blocks run one after another).  Row blocks are multiples of 128
+    rows, so each is a whole number of GEMM tiles, and quantizing x block by
+    block is bit-identical to one call (row partition invariance,
+    /root/reference/pkg/tests/test_quantize.py:371-387).  With world == 1 the
+    GEMM writes ``out`` directly."""
+    m, n_total = out.shape
+    if world == 1:
+        local_gemm(x, w_shard, out)
+        return out
+    step = max(128, -(-(-(-m // chunks)) // 128) * 128)
+    cuda = x.is_cuda and comm_stream is not None
+    compute = torch.cuda.current_stream(x.device) if cuda else None
+    lo, hi = shard_bounds(n_total, world, dist.get_rank(group))
+    for r0 in range(0, m, step):
+        r1 = min(m, r0 + step)
+        local = torch.empty((r1 - r0, hi - lo), dtype=out.dtype, device=out.device)
+        local_gemm(x[r0:r1], w_shard, local)
+        if cuda:
+            ev = torch.cuda.Event()
+            ev.record(compute)
+            with torch.cuda.stream(comm_stream):
+                comm_stream.wait_event(ev)
+                local.record_stream(comm_stream)
+                gather_columns_into(local, out[r0:r1], world, group=group)
+        else:
+            gather_columns_into(local, out[r0:r1], world, group=group)
+    if cuda:
+        compute.wait_stream(comm_stream)
+    return out
+
+
 def column_sharded_linear(x, w_shard, n_total: int, gemm: Callable, world: int, gather: bool = True,
                           group=None) -> torch.Tensor:
     """y = x @ W^T with W split by rows across ranks.  `gemm(x, w_shard)`

@@ -72,3 +72,39 @@ def test_shard_bounds_cover_and_align():
             for lo, hi in spans[:-1]:
                 assert lo % 128 == 0 and (hi - lo) % 128 == 0 or hi == n
     assert P.layer_owner(36, 8)[0] == 0 and P.layer_owner(36, 8)[-1] == 7
+
+
+def _worker_overlap(rank, world, port, results):
+    """column_parallel_forward: row-blocked GEMM + all_gather + (M, N)
+    assembly, against the unsharded product (bit-identical: every element is
+    computed by exactly one rank with the same per-element arithmetic)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import mxq_oracle as O
+        rng = np.random.Generator(np.random.PCG64(1))
+        m, n, k = 300, 700, 256
+        a = rng.standard_t(4, (m, k)).astype(np.float32)
+        w = rng.standard_normal((n, k)).astype(np.float32)
+        lo, hi = P.shard_bounds(n, world, rank)
+        wd = O.dequantize(O.quantize(w[lo:hi], "mbs_d"))
+
+        def local_gemm(x_rows, w_shard, dst):
+            xd = O.dequantize(O.quantize(x_rows.numpy(), "mbs_s"))  # per row block, as on the GPU
+            dst.copy_(torch.from_numpy(O.matmul_blas(xd, w_shard)))
+
+        out = torch.empty((m, n), dtype=torch.float32)
+        P.column_parallel_forward(torch.from_numpy(a), wd, out, world, local_gemm, chunks=3)
+        want = O.matmul_blas(O.dequantize(O.quantize(a, "mbs_s")), O.dequantize(O.quantize(w, "mbs_d")))
+        results[rank] = bool(np.array_equal(out.numpy(), want))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_column_parallel_forward_overlap_gloo_world2():
+    world = 2
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker_overlap, args=(world, _free_port(), results), nprocs=world, join=True)
+    assert all(results[r] for r in range(world))
