@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -217,6 +218,161 @@ __global__ void __launch_bounds__(SQ_THREADS) k_stream_quant(const void* __restr
       const uint32_t t = t0 + u * gridDim.x;
       if (t < ntiles)
         sq_unit<DT, VAR, G>(xb[u], kk[u] < nblk, row_out(q, rr[u]), q.sig_t_ld, kk[u], lane, sig_tab, bad, ovf_any);
+    }
+  }
+  if (bad) atomicOr(status, ST_NONFINITE);
+  if (ovf_any) atomicOr(status, ST_OVERFLOW);
+}
+
+// ---------------------------------------------------------------------------
+// Row-RUN streaming quantizer (K1 / K2 / K4 pass 2, the standalone launches).
+// A thread owns RUN = 4 consecutive 16-element units of one row (64
+// elements): one row pointer per run, four 256-bit loads in flight, and the
+// outputs leave as whole words -- 32 B of codes, the run's 4 scale bytes as
+// one 32-bit store in each layout (row-major and the tcgen05 SF atom, whose 4
+// bytes of a 128-row x 4-block atom row are contiguous), one mantissa byte and
+// one sigma per MBS macro.  Lane j of a warp takes run j of a row, so a warp
+// reads 4 KB contiguous and the per-unit index math of the unit-per-thread
+// form (one unit per lane, ~190 instructions per unit measured) is paid once
+// per run.  MBS macros: UPM = macro/16 units; UPM <= 4 -> RUN/UPM macros per
+// thread, else GL = UPM/4 lanes per macro (max over a lane group); runs per
+// row are padded to a multiple of GL so lane groups never straddle rows.
+// ---------------------------------------------------------------------------
+constexpr int RUN = 4;
+
+template <int DT, int VAR, int UPM>
+__global__ void __launch_bounds__(256) k_quant_runs(const void* __restrict__ x, int64_t x_ld, QDesc q,
+                                                    uint32_t nblk, FastDiv rpr, uint32_t nruns,
+                                                    uint32_t* __restrict__ status) {
+  constexpr int GL = (VAR == SQ_MBS_S && UPM > RUN) ? UPM / RUN : 1;   // lanes per macro
+  constexpr int MPT = (VAR == SQ_MBS_S && UPM <= RUN) ? RUN / UPM : 1;  // macros per thread
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t bad = 0, ovf_any = 0;
+  __shared__ float sig_tab[256];
+  if constexpr (VAR == SQ_MBS_S) {
+    sig_tab[threadIdx.x] = 1.0f / mbs_factor(threadIdx.x);
+    __syncthreads();
+  }
+  const bool words_ok = ((q.scales_ld & 3) == 0) && (((uintptr_t)q.scales & 3) == 0);
+  const uint32_t step = gridDim.x * blockDim.x;
+  const uint32_t total = (nruns + 31u) & ~31u;  // whole warps (GL lane groups stay converged)
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < total; j += step) {
+    const bool live = j < nruns;
+    const uint32_t r = live ? fdiv(j, rpr) : 0u;
+    const uint32_t kb0 = live ? (j - r * rpr.d) * RUN : nblk;
+    const uint32_t nu = kb0 < nblk ? min((uint32_t)RUN, nblk - kb0) : 0u;  // valid units of the run
+    Blk16<DT> xb[RUN];
+    const int64_t off = (int64_t)r * x_ld + (int64_t)kb0 * 16;
+#pragma unroll
+    for (int i = 0; i < RUN; ++i) {
+      if ((uint32_t)i < nu) ld_blk<DT>(x, off + i * 16, xb[i]);
+      else zero_blk<DT>(xb[i]);
+    }
+    float a[RUN];
+#pragma unroll
+    for (int i = 0; i < RUN; ++i) a[i] = blk_absmax<DT>(xb[i], bad);
+    uint32_t codes[RUN][2];
+    uint8_t sc[RUN];
+    uint8_t m8s[MPT];
+    if constexpr (VAR == SQ_MBS_S) {
+      // src/quantize.py:383-406: m8 from the macro max, y = RN(x*f), OAS on y
+#pragma unroll
+      for (int mi = 0; mi < MPT; ++mi) {
+        constexpr int UM = MPT > 1 ? UPM : RUN;  // units of this thread in the macro
+        float am = a[mi * UM];
+#pragma unroll
+        for (int i = 1; i < UM; ++i) am = fmaxf(am, a[mi * UM + i]);
+        if constexpr (GL > 1) am = group_max(am, GL);
+        m8s[mi] = static_m8(am);
+        const float f = mbs_factor(m8s[mi]);
+#pragma unroll
+        for (int i = mi * UM; i < (mi + 1) * UM; ++i) {
+          const float af = __fmul_rn(a[i], f);
+          if ((uint32_t)i < nu && !(af <= 3.402823466e38f)) ovf_any = 1u;
+          const uint8_t biased = e8m0_biased_16(af, true);
+          sc[i] = biased;
+          const float sf = exp2i_f32(127 - (int)biased);
+          float v[16];
+          blk_f32<DT>(xb[i], v);
+          if (biased >= SQ_FOLD_LO && biased <= SQ_FOLD_HI) {
+            // f*SF exact and RN(x*f)*SF == RN(x*(f*SF)) for every element that
+            // can reach a nonzero code (quantizer section)
+            enc16(v, __fmul_rn(f, sf), codes[i]);
+          } else {
+            float y[16];
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) fmul2(y[e], y[e + 1], v[e], v[e + 1], f);
+            enc16(y, sf, codes[i]);
+          }
+        }
+      }
+    } else if constexpr (VAR == SQ_OCP32) {
+#pragma unroll
+      for (int bb = 0; bb < RUN / 2; ++bb) {
+        const uint8_t biased = e8m0_biased_ocp(fmaxf(a[2 * bb], a[2 * bb + 1]));
+        sc[2 * bb] = sc[2 * bb + 1] = biased;
+        const float sf = exp2i_f32(127 - (int)biased);
+#pragma unroll
+        for (int i = 2 * bb; i < 2 * bb + 2; ++i) {
+          float v[16];
+          blk_f32<DT>(xb[i], v);
+          enc16(v, sf, codes[i]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < RUN; ++i) {
+        const uint8_t biased = e8m0_biased_16(a[i], VAR == SQ_OAS);
+        sc[i] = biased;
+        float v[16];
+        blk_f32<DT>(xb[i], v);
+        enc16(v, exp2i_f32(127 - (int)biased), codes[i]);
+      }
+    }
+    if (nu == 0) continue;
+    // ---- stores -------------------------------------------------------------
+    uint8_t* crow = q.codes + (int64_t)r * q.codes_ld + kb0 * 8;
+    if (nu == RUN) {
+      reinterpret_cast<uint4*>(crow)[0] = make_uint4(codes[0][0], codes[0][1], codes[1][0], codes[1][1]);
+      reinterpret_cast<uint4*>(crow)[1] = make_uint4(codes[2][0], codes[2][1], codes[3][0], codes[3][1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < RUN; ++i)
+        if ((uint32_t)i < nu) reinterpret_cast<uint2*>(crow)[i] = make_uint2(codes[i][0], codes[i][1]);
+    }
+    if constexpr (VAR == SQ_OCP32) {
+      // two 32-element blocks per run: scale bytes kb0/2, kb0/2 + 1
+      const uint32_t kbs = kb0 >> 1, ns = (nu + 1) >> 1;
+      if (q.scales) {
+        uint8_t* sp = q.scales + (int64_t)r * q.scales_ld + kbs;
+        for (uint32_t i = 0; i < ns; ++i) sp[i] = sc[2 * i];
+      }
+      if (q.scales_mma) {
+        uint8_t* sp = q.scales_mma + sf_mma_offset(r, kbs, q.sf_kpad);
+        for (uint32_t i = 0; i < ns; ++i) sp[i] = sc[2 * i];
+      }
+    } else {
+      const uint32_t w = (uint32_t)sc[0] | ((uint32_t)sc[1] << 8) | ((uint32_t)sc[2] << 16) | ((uint32_t)sc[3] << 24);
+      if (q.scales) {
+        uint8_t* sp = q.scales + (int64_t)r * q.scales_ld + kb0;
+        if (nu == RUN && words_ok) *reinterpret_cast<uint32_t*>(sp) = w;
+        else for (uint32_t i = 0; i < nu; ++i) sp[i] = sc[i];
+      }
+      if (q.scales_mma) {  // kb0 % 4 == 0: the 4 bytes of one atom row are contiguous
+        uint8_t* sp = q.scales_mma + sf_mma_offset(r, kb0, q.sf_kpad);
+        if (nu == RUN) *reinterpret_cast<uint32_t*>(sp) = w;
+        else for (uint32_t i = 0; i < nu; ++i) sp[i] = sc[i];
+      }
+      if constexpr (VAR == SQ_MBS_S) {
+#pragma unroll
+        for (int mi = 0; mi < MPT; ++mi) {
+          const uint32_t ufirst = kb0 + mi * (MPT > 1 ? UPM : RUN);
+          if (ufirst >= nblk || (GL > 1 && (lane & (GL - 1)) != 0)) continue;
+          const uint32_t mac = ufirst / UPM;
+          if (q.mant) q.mant[(int64_t)r * q.mant_ld + mac] = m8s[mi];
+          if (q.sig_t) q.sig_t[(int64_t)mac * q.sig_t_ld + r] = sig_tab[m8s[mi]];
+        }
+      }
     }
   }
   if (bad) atomicOr(status, ST_NONFINITE);
@@ -592,21 +748,41 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
   const int64_t ntiles64 = rows * (int64_t)tpr_n;
   if (ntiles64 >= (int64_t)1 << 31) return set_error(ERR_UNSUPPORTED, "tensor too large");
   const uint32_t ntiles = (uint32_t)ntiles64;
-  const int sq_grid = (int)std::min<int64_t>((ntiles + SQ_UNROLL - 1) / SQ_UNROLL, (int64_t)num_sms() * 8);
-#define SQ_LAUNCH(VAR, G)                                                                                        \
+#ifndef MXQ_SQ_CTAS
+#define MXQ_SQ_CTAS 8
+#endif
+  const int sq_grid = (int)std::min<int64_t>((ntiles + SQ_UNROLL - 1) / SQ_UNROLL, (int64_t)num_sms() * MXQ_SQ_CTAS);
+  // row-run launches: runs per row padded to a multiple of the MBS lane group
+  const uint32_t runs_raw = (nblk + RUN - 1) / RUN;
+#define UNIT_LAUNCH(VAR, G)                                                                                     \
   do {                                                                                                          \
     if (bf) k_stream_quant<DT_BF16, VAR, G><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status); \
     else k_stream_quant<DT_F32, VAR, G><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status);     \
   } while (0)
+#define RUN_LAUNCH(VAR, UPM)                                                                                     \
+  do {                                                                                                          \
+    constexpr uint32_t GLV = (VAR == SQ_MBS_S && UPM > RUN) ? UPM / RUN : 1;                                    \
+    const uint32_t rpr_n = (runs_raw + GLV - 1) / GLV * GLV;                                                    \
+    const int64_t nr = rows * (int64_t)rpr_n;                                                                   \
+    if (nr >= ((int64_t)1 << 31) - 32) return set_error(ERR_UNSUPPORTED, "tensor too large");                   \
+    const int grid = (int)std::min<int64_t>((nr + 255) / 256, (int64_t)num_sms() * MXQ_SQ_CTAS);                \
+    if (bf) k_quant_runs<DT_BF16, VAR, UPM><<<grid, 256, 0, st>>>(x, x_ld, q, nblk, make_fastdiv(rpr_n),       \
+                                                                  (uint32_t)nr, status);                        \
+    else k_quant_runs<DT_F32, VAR, UPM><<<grid, 256, 0, st>>>(x, x_ld, q, nblk, make_fastdiv(rpr_n),           \
+                                                              (uint32_t)nr, status);                            \
+  } while (0)
   switch (q.variant) {
+    // OCP32 / MX16 / OAS: one 16-element unit per lane (k_stream_quant); MBS-S:
+    // a run of four units per thread (k_quant_runs) -- the faster form of each
+    // (quantizer section: measured unit / run / TMA-staged forms)
     case OCP32:
-      SQ_LAUNCH(SQ_OCP32, 2);
+      UNIT_LAUNCH(SQ_OCP32, 2);
       break;
     case MX16:
-      SQ_LAUNCH(SQ_MX16, 1);
+      UNIT_LAUNCH(SQ_MX16, 1);
       break;
     case MX16_OAS:
-      SQ_LAUNCH(SQ_OAS, 1);
+      UNIT_LAUNCH(SQ_OAS, 1);
       break;
     case MBS_S:
     case MBS_D: {
@@ -617,13 +793,13 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
       const int64_t ngroups = rows * g.nmac;
       if (q.variant == MBS_S && g.G * 16 == g.macro) {
-        switch (g.G) {  // power-of-two macro: G lanes per macro inside the row tile
-          case 1: SQ_LAUNCH(SQ_MBS_S, 1); break;
-          case 2: SQ_LAUNCH(SQ_MBS_S, 2); break;
-          case 4: SQ_LAUNCH(SQ_MBS_S, 4); break;
-          case 8: SQ_LAUNCH(SQ_MBS_S, 8); break;
-          case 16: SQ_LAUNCH(SQ_MBS_S, 16); break;
-          default: SQ_LAUNCH(SQ_MBS_S, 32); break;
+        switch (g.G) {  // power-of-two macro of G units
+          case 1: RUN_LAUNCH(SQ_MBS_S, 1); break;
+          case 2: RUN_LAUNCH(SQ_MBS_S, 2); break;
+          case 4: RUN_LAUNCH(SQ_MBS_S, 4); break;
+          case 8: RUN_LAUNCH(SQ_MBS_S, 8); break;
+          case 16: RUN_LAUNCH(SQ_MBS_S, 16); break;
+          default: RUN_LAUNCH(SQ_MBS_S, 32); break;
         }
       } else if (q.variant == MBS_S) {
         const FastDiv fd = make_fastdiv((uint32_t)g.nmac);

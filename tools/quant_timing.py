@@ -31,3 +31,14 @@ for v, bpe in ((V.OCP32, 2.53125), (V.MX16, 2.5625), (V.MX16_OAS, 2.5625), (V.MB
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     print(f"{v.value:9s} {n}x{ncol} {ms*1e3:7.2f} us  {n*ncol*bpe/ms/1e6:7.0f} GB/s (HBM-cold inputs)", flush=True)
+# reference: a device copy of the same bf16 tensor (read + write 2 B/elem each)
+dst = torch.empty_like(xs[0])
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph):
+    for i in range(48):
+        dst.copy_(xs[i % 8])
+graph.replay(); torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record(); graph.replay(); e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 48
+print(f"copy      {n}x{ncol} {ms*1e3:7.2f} us  {n*ncol*4/ms/1e6:7.0f} GB/s (torch copy_, read+write)", flush=True)
