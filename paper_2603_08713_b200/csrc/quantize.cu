@@ -379,6 +379,175 @@ __global__ void __launch_bounds__(256) k_quant_runs(const void* __restrict__ x, 
   if (ovf_any) atomicOr(status, ST_OVERFLOW);
 }
 
+// ---------------------------------------------------------------------------
+// K4 NVFP4 in the run form (src/quantize.py:662-706): pass 1 |x| max, pass 2
+// E4M3 block scale + element codes, four 16-element units per thread.
+// Block scale: the E4M3 RNE code of the f64 ratio alpha / (6 s_t) is taken from
+// the hardware converter on an f32 estimate (relative error < 2^-22) at
+// r(1 - 2^-19), r and r(1 + 2^-19); when the three codes agree they equal the
+// code of the exact ratio (E4M3 RNE is monotone), else the f64 division runs.
+// Elements: as nvfp4_unit (f32 estimate, three E2M1 encodes, f64 fallback).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cvt_e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// Warp CHUNKS: a warp takes 128 consecutive units of one row (lane: units
+// base + lane + 32 i), so every 256-bit load instruction reads 1 KB contiguous
+// (a run of four units per lane reads a 4 KB span per instruction: 4x the L1
+// tag work per byte) and the row pointer is computed once per chunk.
+constexpr int CHUNK = 128;
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_absmax_runs(const void* __restrict__ x, int64_t x_ld, uint32_t nblk,
+                                                     FastDiv cpr, uint32_t nchunks, uint32_t* __restrict__ status) {
+  uint32_t bad = 0;
+  float m = 0.0f;
+  const uint32_t lane = threadIdx.x & 31, wstep = gridDim.x * (blockDim.x / 32);
+  for (uint32_t ch = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); ch < nchunks; ch += wstep) {
+    const uint32_t r = fdiv(ch, cpr), kb0 = (ch - r * cpr.d) * CHUNK;
+    Blk16<DT> xb[CHUNK / 32];
+#pragma unroll
+    for (int i = 0; i < CHUNK / 32; ++i) {
+      const uint32_t kb = kb0 + lane + 32 * i;
+      if (kb < nblk) ld_blk<DT>(x, (int64_t)r * x_ld + (int64_t)kb * 16, xb[i]);
+      else zero_blk<DT>(xb[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < CHUNK / 32; ++i) m = fmaxf(m, blk_absmax<DT>(xb[i], bad));
+  }
+  // one atomic per CTA, and only when it can raise the running maximum
+  // (same-address atomics of one per warp serialize at the L2 slice)
+  __shared__ uint32_t s_m, s_bad;
+  if (threadIdx.x == 0) { s_m = 0u; s_bad = 0u; }
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if (lane == 0) {
+    atomicMax(&s_m, __float_as_uint(m));
+    if (bad) atomicOr(&s_bad, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t mb = s_m;
+    if (mb != 0u && mb > *reinterpret_cast<volatile uint32_t*>(status + 1)) atomicMax(status + 1, mb);
+    if (s_bad) atomicOr(status, ST_NONFINITE);
+  }
+}
+
+// Rare exact paths, out of line so the hot loop stays small (an inlined f64
+// division per call site overflowed the instruction cache: 44 % of the stall
+// samples were no_instructions).
+__device__ __noinline__ uint32_t nvfp4_scale_exact(float alpha, double six_st) {
+  return e4m3_code_f64((double)alpha / six_st);
+}
+__device__ __noinline__ uint32_t nvfp4_pair_exact(float v0, float v1, double st, uint32_t sb) {
+  const double den = st * e4m3_decode(sb);
+  return e2m1_code_f64(__ddiv_rn((double)v0, den)) | (e2m1_code_f64(__ddiv_rn((double)v1, den)) << 4);
+}
+// E4M3 value of a code (0..0x7E) as an exact f32.
+__device__ __forceinline__ float e4m3_f32(uint32_t c) {
+  const uint32_t e = c >> 3, m = c & 7u;
+  return e ? __uint_as_float(((e + 120u) << 23) | (m << 20)) : (float)m * 0.001953125f;  // subnormal: m * 2^-9
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) k_nvfp4_runs(const void* __restrict__ x, int64_t x_ld, QDesc q, uint32_t nblk,
+                                                    FastDiv cpr, uint32_t nchunks,
+                                                    const uint32_t* __restrict__ amax_bits) {
+  const float amax = __uint_as_float(*amax_bits);
+  const bool nz = amax > 0.0f;
+  const double st = nz ? (double)amax / 2688.0 : 1.0;
+  const double six_st = 6.0 * st;
+  const float inv6 = (float)(1.0 / six_st);
+  const bool est_ok = inv6 >= 1.17549435e-38f && inv6 <= 3.0e38f;  // f32-normal reciprocal (else f64 scales)
+  const float st32 = (float)st;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && q.tensor_scale) *q.tensor_scale = st;
+  const uint32_t lane = threadIdx.x & 31, wstep = gridDim.x * (blockDim.x / 32);
+  for (uint32_t ch = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); ch < nchunks; ch += wstep) {
+    const uint32_t r = fdiv(ch, cpr), kb0 = (ch - r * cpr.d) * CHUNK;
+    constexpr int NU = CHUNK / 32;
+    Blk16<DT> xb[NU];
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      const uint32_t kb = kb0 + lane + 32 * i;
+      if (kb < nblk) ld_blk<DT>(x, (int64_t)r * x_ld + (int64_t)kb * 16, xb[i]);
+      else zero_blk<DT>(xb[i]);
+    }
+    uint32_t codes[NU][2];
+    uint32_t scw = 0;
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      uint32_t unused = 0;
+      const float alpha = blk_absmax<DT>(xb[i], unused);
+      uint32_t sb = 0;
+      if (nz) {
+        const float rr = alpha * inv6;
+        const uint32_t c2 = cvt_e4m3x2(rr * 0.99999809265136719f, rr * 1.00000190734863281f);  // r (1 -+ 2^-19)
+        const uint32_t cm = cvt_e4m3x2(rr, rr) & 0xFFu;
+        sb = (est_ok && (c2 & 0xFFu) == cm && (c2 >> 8) == cm) ? cm : nvfp4_scale_exact(alpha, six_st);
+      }
+      scw |= sb << (8 * i);
+      codes[i][0] = codes[i][1] = 0u;
+      if (sb != 0) {
+        // quotient estimate x / den in f32: den32 = RN(RN(st) * E4M3(sb)), relative
+        // error < 2^-21 after the reciprocal and the product
+        const float den32 = st32 * e4m3_f32(sb);
+        const bool f32_ok = den32 > 1e-30f && den32 < 1e30f;
+        const float inv = __frcp_rn(den32);
+        // the exact quotient lies between x*inv_lo and x*inv_hi (relative error
+        // of the estimate < 2^-21 << 2^-17); E2M1 RNE is monotone, so equal
+        // codes at both ends are the code of the exact quotient
+        const float inv_lo = inv * 0.99999237060546875f, inv_hi = inv * 1.00000762939453125f;  // 1 -+ 2^-17
+        float v[16];
+        blk_f32<DT>(xb[i], v);
+        uint32_t word[2] = {0u, 0u}, mism = 0;  // mism: pairs whose two ends disagree
+#pragma unroll
+        for (int pr = 0; pr < 8; ++pr) {
+          float l0, l1, u0, u1;
+          fmul2(l0, l1, v[2 * pr], v[2 * pr + 1], inv_lo);
+          fmul2(u0, u1, v[2 * pr], v[2 * pr + 1], inv_hi);
+          const uint32_t c = cvt_e2m1x2(l0, l1);
+          mism |= (cvt_e2m1x2(u0, u1) != c) ? (1u << pr) : 0u;
+          word[pr >> 2] |= c << (8 * (pr & 3));
+        }
+        if (!f32_ok) mism = 0xFFu;
+        // straddling pairs (f64 quotient, out of line).  On bf16 data about 0.4 %
+        // of the elements sit EXACTLY on an E2M1 midpoint after the f64 division
+        // (x, amax and the E4M3 scale have few significand bits), so most warps
+        // take this branch for a pair or two per unit -- it is the main cost of
+        // the pass (NVFP4).
+        if (mism) {
+          for (int pr = 0; pr < 8; ++pr)
+            if (mism & (1u << pr)) {
+              const uint32_t c = nvfp4_pair_exact(v[2 * pr], v[2 * pr + 1], st, sb);
+              word[pr >> 2] = (word[pr >> 2] & ~(0xFFu << (8 * (pr & 3)))) | (c << (8 * (pr & 3)));
+            }
+        }
+        codes[i][0] = fix_neg_zero(word[0]);
+        codes[i][1] = fix_neg_zero(word[1]);
+      }
+    }
+    uint8_t* crow = q.codes + (int64_t)r * q.codes_ld;
+    uint8_t* srow = q.scales ? q.scales + (int64_t)r * q.scales_ld : nullptr;
+    uint8_t* mrow = q.scales_mma ? q.scales_mma + sf_mma_offset(r, 0, q.sf_kpad) : nullptr;
+#pragma unroll
+    for (int i = 0; i < NU; ++i) {
+      const uint32_t kb = kb0 + lane + 32 * i;
+      if (kb < nblk) {
+        *reinterpret_cast<uint2*>(crow + kb * 8) = make_uint2(codes[i][0], codes[i][1]);
+        const uint8_t sb = (uint8_t)(scw >> (8 * i));
+        if (srow) srow[kb] = sb;
+        if (mrow) mrow[(kb >> 2) * 512u + (kb & 3u)] = sb;
+      }
+    }
+  }
+}
+
 // K4 pass 1: |x| max of the whole tensor (uint ordering of non-negative
 // floats) and the non-finite check, same tiling, one atomic per warp.
 template <int DT>
@@ -821,17 +990,21 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       break;
     }
     case NVFP4: {
-      const int64_t nb = rows * (cols / 16);
+      // pass 1 |x| max into status[1], pass 2 scales and codes (run form)
       cudaError_t e = cudaMemsetAsync(status + 1, 0, sizeof(uint32_t), st);
       if (e != cudaSuccess) return set_cuda_error(e);
-      (void)nb;
-      const int nv_grid = (int)std::min<int64_t>((ntiles + 1) / 2, (int64_t)num_sms() * 8);
+      const uint32_t cpr_n = (nblk + CHUNK - 1) / CHUNK;
+      const int64_t nch = rows * (int64_t)cpr_n;
+      if (nch >= ((int64_t)1 << 31)) return set_error(ERR_UNSUPPORTED, "tensor too large");
+      const int grid = (int)std::min<int64_t>((nch + 7) / 8, (int64_t)num_sms() * MXQ_SQ_CTAS);
+      const FastDiv fr = make_fastdiv(cpr_n);
+      const uint32_t nr = (uint32_t)nch;
       if (bf) {
-        k_stream_absmax<DT_BF16><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, nblk, tpr, ntiles, status);
-        k_stream_nvfp4<DT_BF16><<<nv_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status + 1);
+        k_absmax_runs<DT_BF16><<<grid, 256, 0, st>>>(x, x_ld, nblk, fr, (uint32_t)nr, status);
+        k_nvfp4_runs<DT_BF16><<<grid, 256, 0, st>>>(x, x_ld, q, nblk, fr, (uint32_t)nr, status + 1);
       } else {
-        k_stream_absmax<DT_F32><<<sq_grid, SQ_THREADS, 0, st>>>(x, x_ld, nblk, tpr, ntiles, status);
-        k_stream_nvfp4<DT_F32><<<nv_grid, SQ_THREADS, 0, st>>>(x, x_ld, q, nblk, tpr, ntiles, status + 1);
+        k_absmax_runs<DT_F32><<<grid, 256, 0, st>>>(x, x_ld, nblk, fr, (uint32_t)nr, status);
+        k_nvfp4_runs<DT_F32><<<grid, 256, 0, st>>>(x, x_ld, q, nblk, fr, (uint32_t)nr, status + 1);
       }
       break;
     }
