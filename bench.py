@@ -280,6 +280,7 @@ def run_ours(args):
     # the timed launches cycle over 8 distinct activations (256 MB, twice the
     # L2), so every launch streams its input from HBM
     qbw = quantizer_bandwidth(torch, M, dev, args)
+    experts = grouped_experts(torch, M, dev, args) if (rank == 0 and args.experts) else None
 
     out = None
     if rank == 0:
@@ -339,6 +340,7 @@ def run_ours(args):
         "mbs_h_overhead_vs_nvfp4": round(1.0 - head["tflops_step"] / results["nvfp4"]["tflops_step"], 4),
         "quantizer": {k: {kk: round(vv, 2) for kk, vv in v.items()} for k, v in qbw.items()},
         "quantizer_hbm_frac_mbs_s": round(qbw["mbs_s"]["gbs"] / hbm_peak(), 4),
+        "moe_experts_c5": experts,
         "qsnr_config1": out["qsnr"],
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -435,7 +437,78 @@ def quantizer_bandwidth(torch, M, dev, args):
         qbw[vname] = {"us": ms * 1e3, "gbs": xq[0].numel() * bytes_per_el[vname] / (ms * 1e-3) / 1e9,
                       "melem_s": xq[0].numel() / (ms * 1e-3) / 1e6}
     del xq
+    # the same kernels on the down-projection's activation (4096 x 14336, 117 MB
+    # bf16): at 32 MB a pure-read kernel reaches only ~4.1 TB/s on this part
+    # (tools/microbench_read.cu: ~3 us of per-launch ramp), so the config-size
+    # fraction is reported beside the 4096^2 one
+    xl = [torch.randn(M_TOK, 14336, device=dev, generator=gq).to(torch.bfloat16) for _ in range(3)]
+    for vname in ("mx16_oas", "mbs_s", "nvfp4"):
+        cfg = M.SchemeConfig(V(vname))
+        for x in xl:
+            M.quantize_tensor(x, cfg, check=False, gemm_layout=True)
+        torch.cuda.synchronize()
+        reps = 12
+        g = torch.cuda.CUDAGraph()  # device time of the launches alone (no host gaps)
+        with torch.cuda.graph(g):
+            for i in range(reps):
+                M.quantize_tensor(xl[i % 3], cfg, check=False, gemm_layout=True)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        qbw[vname + "@4096x14336"] = {"us": ms * 1e3, "gbs": xl[0].numel() * bytes_per_el[vname] / (ms * 1e-3) / 1e9,
+                                      "melem_s": xl[0].numel() / (ms * 1e-3) / 1e6}
+    del xl
     return qbw
+
+
+def grouped_experts(torch, M, dev, args):
+    """C5: GPT-OSS-120B MoE expert GEMMs (decode-sized token groups), 64
+    experts per launch, MBS-H (MBS_S tokens x MBS_D weights) vs NVFP4 x NVFP4,
+    both on the grouped tcgen05 kernel (matmul_quantized_grouped).  The 64
+    experts' weights (gate_up 5760 x 2880: 597 MB in MBS) exceed the L2, so
+    every launch streams its weights from HBM; reported as weight GB/s
+    (algorithmic weight bytes: codes + scales + MBS mantissa bytes) and
+    microseconds per expert."""
+    V = M.Variant
+    n_exp, k = 64, 2880
+    out = {}
+    hbm = hbm_peak()
+    for proj, n in (("gate_up", 5760), ("down", 2880)):
+        gw = torch.Generator(device=dev).manual_seed(777)
+        wd = [(torch.randn(n, k, device=dev, generator=gw) * 0.02).to(torch.bfloat16) for _ in range(n_exp)]
+        for arm, (av, wv) in (("mbs_h", (V.MBS_S, V.MBS_D)), ("nvfp4", (V.NVFP4, V.NVFP4))):
+            wq = [M.quantize_tensor(w, M.SchemeConfig(wv), check=False) for w in wd]
+            wbytes = n * k * (0.5 + 1 / 16 + (1 / 128 if arm == "mbs_h" else 0.0))
+            for mtok in (1, 8, 32, 128):
+                gt = torch.Generator(device=dev).manual_seed(mtok)
+                toks = [M.quantize_tensor(torch.randn(mtok, k, device=dev, generator=gt).to(torch.bfloat16),
+                                          M.SchemeConfig(av), check=False) for _ in range(n_exp)]
+                M.matmul_quantized_grouped(toks, wq, out_dtype=torch.bfloat16, check=False)
+                torch.cuda.synchronize()
+                reps = 10
+                g = torch.cuda.CUDAGraph()  # device time of the launches (the expert table is a kernel parameter)
+                with torch.cuda.graph(g):
+                    for _ in range(reps):
+                        M.matmul_quantized_grouped(toks, wq, out_dtype=torch.bfloat16, check=False)
+                g.replay()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                g.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                us = e0.elapsed_time(e1) / reps * 1e3
+                gbs = n_exp * wbytes / (us * 1e-6) / 1e9
+                out[f"{proj}.{arm}.m{mtok}"] = {"us_per_launch": round(us, 2), "us_per_expert": round(us / n_exp, 3),
+                                                "weight_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 3)}
+            del wq
+        del wd
+    return out
 
 
 def run_e2e(torch, M, P, dev, world, args, acts, outs, wq, step_flops_global, barrier, n_layers, cols):
@@ -711,6 +784,8 @@ def main():
     ap.add_argument("--workload", default="llama8b", choices=tuple(WORKLOADS),
                     help="llama8b: the four Llama-3-8B linears (C2); llama70b-ffn: the 70B FFN gate/up (C4)")
     ap.add_argument("--chunks", type=int, default=4, help="columns mode: row blocks of the gather overlap")
+    ap.add_argument("--no-experts", dest="experts", action="store_false",
+                    help="skip the C5 grouped expert-GEMM block (MBS-H vs NVFP4)")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-wrows", type=int, default=2048)

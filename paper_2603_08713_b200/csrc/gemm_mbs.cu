@@ -146,6 +146,8 @@ struct GroupDesc {
   void* c;
   int n;                 // kernel N of this group (tokens, swap-AB form)
   int m;                 // kernel M of this group (tokens, direct form)
+  const double* tsa;     // NVFP4 groups: the two tensor scales (s_t of each operand), else null
+  const double* tsb;
 };
 struct GroupTable {
   Params p;
@@ -605,6 +607,16 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
       // store the tile row (masked to M x N): the output, or this split's f32 partial
       void* const cout = GROUPED ? gt->g[U.g].c : p.c;
       const int n_out = GROUPED ? gt->g[U.g].n : p.N;
+      if constexpr (GROUPED) {
+        // NVFP4 groups: C = s_tA s_tB (sum of the UE4M3-scaled products), the
+        // plain NVFP4 kernel's epilogue (src/quantize.py:409-423 applies s_t per element)
+        const GroupDesc& G = gt->g[U.g];
+        if (G.tsa) {
+          const float ts = (float)(*G.tsa * *G.tsb);
+#pragma unroll
+          for (int i = 0; i < COLS; ++i) acc[i] *= ts;
+        }
+      }
       if (TRANS && row < p.M) {
         // kernel row = weight row n, kernel column = token: C[token][n] (and the
         // split partials in the same output orientation)
@@ -1339,12 +1351,21 @@ static int launch_grouped(const QDesc* ka, const QDesc* kb, void* const* c, int 
     p.M = kernel_m;
     p.N = kernel_n;
     p.K = (int)a.cols;
-    const int macro = ma ? a.macro_size : b.macro_size;
-    p.mac_steps = macro / KSTEP;
-    p.n_chunks = (int)((a.cols + macro - 1) / macro);
+    const bool nv = a.variant == NVFP4;  // (grouped NVFP4: both sides NVFP4, checked by the caller)
+    if (ma || mbb) {
+      const int macro = ma ? a.macro_size : b.macro_size;
+      p.mac_steps = macro / KSTEP;
+      p.n_chunks = (int)((a.cols + macro - 1) / macro);
+    } else {
+      // no MBS side: one chunk spanning K -- the MMAs accumulate the whole
+      // reduction in TMEM and the epilogue folds once (sigma = 1)
+      p.mac_steps = (int)((a.cols + KSTEP - 1) / KSTEP);
+      p.n_chunks = 1;
+    }
     p.ksplit = 1;
     p.trace = nullptr;
-    p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+    // E2M1 x E2M1, N = BN, M = 128; scale format UE8M0 (bit 23) or UE4M3 (NVFP4)
+    p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((nv ? 0u : 1u) << 23) | ((uint32_t)(BM >> 4) << 24);
     t->n_groups = ng;
     for (int j = 0; j < ng; ++j) {
       const QDesc& ag = ka[g0 + j];
@@ -1362,6 +1383,8 @@ static int launch_grouped(const QDesc* ka, const QDesc* kb, void* const* c, int 
       G.c = c[g0 + j];
       G.n = TRANS ? (int)bg.rows : kernel_n;
       G.m = TRANS ? kernel_m : (int)ag.rows;
+      G.tsa = nv ? ag.tensor_scale : nullptr;
+      G.tsb = nv ? bg.tensor_scale : nullptr;
     }
     const int units = ng * (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
     const int clusters = std::min(units, num_sms() / CL);
@@ -1482,10 +1505,13 @@ int launch_gemm_mbs_grouped(const QDesc* a, const QDesc* b, int n, void* const* 
                             cudaStream_t st) {
   if (n < 1) return set_error(ERR_INVALID, "no groups");
   int max_tok = 0;
+  const bool nv = a[0].variant == NVFP4 && b[0].variant == NVFP4;
   for (int g = 0; g < n; ++g) {
     const QDesc& x = a[g];
     const QDesc& w = b[g];
-    if (!gemm_mbs_supported(x, w) || x.rows < 1 || x.rows > 128 || w.rows < 256 || x.cols != w.cols ||
+    const bool pair_ok = nv ? (x.variant == NVFP4 && w.variant == NVFP4 && x.tensor_scale && w.tensor_scale)
+                            : gemm_mbs_supported(x, w);
+    if (!pair_ok || x.rows < 1 || x.rows > 128 || w.rows < 256 || x.cols != w.cols ||
         w.rows != b[0].rows || w.cols != b[0].cols || w.variant != b[0].variant || x.variant != a[0].variant ||
         w.macro_size != b[0].macro_size || x.macro_size != a[0].macro_size || w.sf_kpad != b[0].sf_kpad ||
         x.sf_kpad != a[0].sf_kpad || w.sig_t_ld != b[0].sig_t_ld || x.sig_t_ld != a[0].sig_t_ld ||

@@ -174,11 +174,13 @@ def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dt
     """``[matmul_quantized(a, b) for a, b in zip(aqs, bqs)]`` for MoE-style
     expert GEMMs (SURVEY section 8 d config 5): ``aqs[g]`` the tokens routed
     to expert g (at most 128 rows for the grouped kernel), ``bqs[g]`` that
-    expert's weights, all of one shape.  MBS / E8M0 pairs of one variant pair
-    run as one launch of the MBS kernel per 64 experts (swap-AB up to 64
-    tokens, direct 128-row tiles up to 128)
-    (csrc/gemm_mbs.cu ``k_gemm_mbs_grouped``); other pairs fall back to one
-    launch per expert.  Tolerance parity as ``matmul_quantized``."""
+    expert's weights, all of one shape.  MBS pairs (MBS-H: MBS_S tokens x
+    MBS_D weights, or an MBS side against E8M0) and NVFP4 x NVFP4 pairs run
+    as one launch per 64 experts (swap-AB up to 64 tokens, direct 128-row
+    tiles up to 128) (csrc/gemm_mbs.cu ``k_gemm_mbs_grouped``; NVFP4 groups
+    use UE4M3 scales, one K chunk and the s_tA s_tB epilogue); other pairs
+    fall back to one launch per expert.  Tolerance parity as
+    ``matmul_quantized``."""
     aqs, bqs = list(aqs), list(bqs)
     if len(aqs) != len(bqs) or not aqs:
         raise ValueError("need one weight per token group")
@@ -192,11 +194,18 @@ def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dt
         _validate_chunking(bq, cfg.t_k, "b")
     if out_dtype not in (torch.float32, torch.bfloat16):
         raise ValueError("out_dtype must be float32 or bfloat16")
-    # the grouped kernel takes MBS pairs (block-16 scale layout); anything else
-    # runs expert by expert through matmul_quantized
-    if not all(tc_supported(aq, bq) and (aq.mbs_mantissas is not None or bq.mbs_mantissas is not None)
-               and Variant.NVFP4 not in (aq.variant, bq.variant) for aq, bq in zip(aqs, bqs)):
+    # the grouped kernel takes MBS pairs and NVFP4 x NVFP4 pairs (block-16 scale
+    # layouts); anything else runs expert by expert through matmul_quantized
+    def grouped_pair(aq, bq):
+        if aq.variant is Variant.NVFP4 or bq.variant is Variant.NVFP4:
+            return aq.variant is Variant.NVFP4 and bq.variant is Variant.NVFP4
+        return tc_supported(aq, bq) and (aq.mbs_mantissas is not None or bq.mbs_mantissas is not None)
+
+    if not all(grouped_pair(aq, bq) for aq, bq in zip(aqs, bqs)):
         return [matmul_quantized(aq, bq, cfg, out_dtype=out_dtype, check=check) for aq, bq in zip(aqs, bqs)]
+    if check:
+        for q in (*aqs, *bqs):
+            _check_scale_codes(q)
     dev = aqs[0].codes.device
     outs = [torch.empty((aq.shape[0], n), dtype=out_dtype, device=dev) for aq in aqs]
     sfb = 16  # (an MBS operand makes every pair block-16)

@@ -221,7 +221,9 @@ def test_quantize_matmul_fused_repeated_and_nonfinite():
     ([2, 9], 512, 1024, "mx16_oas", "mbs_s", torch.float32),          # non-MBS weights
     ([100, 128, 65], 640, 2880, "mbs_d", "mbs_s", torch.float32),     # direct form (65-128 tokens)
     ([128] * 3, 384, 1024, "mbs_d", "mbs_s", torch.bfloat16),
-    ([4, 4], 512, 1024, "nvfp4", "nvfp4", torch.float32),             # per-group fallback
+    ([4, 4], 512, 1024, "nvfp4", "nvfp4", torch.float32),             # grouped NVFP4 (UE4M3, swap-AB)
+    ([1, 8, 32, 64], 1280, 2880, "nvfp4", "nvfp4", torch.bfloat16),   # GPT-OSS K, decode sizes
+    ([100, 128], 640, 2880, "nvfp4", "nvfp4", torch.float32),         # grouped NVFP4, direct form
 ])
 def test_grouped_expert_gemm_matches_reference(toks, n, k, wv, av, out_dtype):
     g = torch.Generator(device="cuda").manual_seed(11 + len(toks) + n)
