@@ -160,19 +160,11 @@ struct GroupTable {
 #endif
 // 16 clock64 slots per chunk of CTA 0, first 512 chunks (tools/trace_mbs.py).
 __device__ __forceinline__ void trace_at(const Params& p, uint32_t chunk, int slot) {
-  if constexpr (MXQ_GEMM_TRACE == 1) {
+  if constexpr (MXQ_GEMM_TRACE != 0) {
     if (p.trace != nullptr && blockIdx.x == 0 && chunk < 512 && (threadIdx.x & 31) == 0)
       p.trace[chunk * 16 + slot] = clock64();
   }
 }
-// MXQ_GEMM_TRACE == 2: per-warp release / fold-end times (slots warp, 8 + warp)
-__device__ __forceinline__ void trace2_at(const Params& p, uint32_t chunk, int slot) {
-  if constexpr (MXQ_GEMM_TRACE == 2) {
-    if (p.trace != nullptr && blockIdx.x == 0 && chunk < 512 && (threadIdx.x & 31) == 0)
-      p.trace[chunk * 16 + slot] = clock64();
-  }
-}
-
 template <int R>
 __device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R)); }
 template <int R>
@@ -556,6 +548,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         if (warp == 0) trace_at(p, q, 3);
         mbar_wait_a(a_tfull + b * 8, tp);
         if (warp == 0) trace_at(p, q, 4);
+        if (warp == EPIW - 1) trace_at(p, q, 8);
         tc_fence_after();
         float v[COLS];
 #pragma unroll
@@ -585,6 +578,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           fma2(acc[i + 2], acc[i + 3], w2, w3, v[i + 2], v[i + 3]);
         }
         if (warp == 0) trace_at(p, q, 7);
+        if (warp == EPIW - 1) trace_at(p, q, 9);
         ++q;
       };
       int c = U.c_lo;
@@ -694,458 +688,6 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
   }
 }
 
-// ===========================================================================
-// Prefill-shape MBS GEMM (round 2): 128 x 128 tiles, three TMEM partial
-// buffers, eight epilogue warps with register double-buffered partials.
-//
-// Per 128-K chunk and SM: 256 cycles of FP32 fold (2 ops x 128 x 128 / 128
-// lanes), 128 of MMA, ~163 of MMA-warp issue (2 MMAs + 4 SF copies + a commit,
-// tools/microbench_issue.cu) and ~180 of TMEM reads (64 KB at ~360 B/clk).
-// The fold is the bound; everything else must hide under it:
-//   * each epilogue warp owns 32 rows x 64 columns of the tile and reads its
-//     partial with tcgen05.ld 16x256b, so a thread holds 4 rows x 16 columns:
-//     the chunk's sigma_B slice is 16 registers (8 LDS.64) and sigma_A 4, and
-//     the fold is FMUL2(P pair, sigma_B pair) + FFMA2(u, sigma_A, acc) with no
-//     shared-memory operand (82 % of the FP32 pipe in isolation against 71 %
-//     for a sigma_B LDS.128 per four columns, tools/microbench_fold.cu);
-//   * it starts the TMEM load of chunk c+1 into a second register set before
-//     folding chunk c and releases a partial buffer as soon as its registers
-//     hold it; the barrier tests for the next chunk are issued before the fold
-//     and consumed after it (mbarrier.test_wait), so their latency runs under
-//     the FP32 work;
-//   * three partial buffers let the MMA run two chunks ahead;
-//   * sigma arrives once per 256-K stage (one ring slot holds the stage's
-//     chunks), not once per chunk;
-//   * clusters of 2 CTAs along M share each B tile by TMA multicast.
-// ===========================================================================
-#ifndef MXQ_MBS2_EXP
-#define MXQ_MBS2_EXP 0  // development knock-out bitmask (tools/build_variant.sh): 1 fold, 2 TMEM loads, 4 MMAs, 8 sigma ring, 16 SF copies
-#endif
-#ifndef MXQ_MBS2_STAGES
-#define MXQ_MBS2_STAGES 0
-#endif
-template <bool PAIR>
-struct Mbs2Cfg {
-  static constexpr int BN = 128, NB = 3, EPIW = 8;
-  static constexpr int W_TMA = EPIW, W_MMA = EPIW + 1;
-  static constexpr int THREADS = (EPIW + 4) * 32;      // 8 epilogue warps + one control warpgroup
-  static constexpr int STAGE_B = (PAIR ? BN / 2 : BN) * KSTAGE / 2;  // this CTA's B rows: 16 KB, 8 KB in a pair
-  static constexpr int STAGES = MXQ_MBS2_STAGES ? MXQ_MBS2_STAGES : (PAIR ? 7 : 5);
-  static constexpr int SFB_BYTES = 4 * ATOM;           // one 128-row atom x 4 k-steps
-  static constexpr int NSIG = 4, SIGC = 4;             // sigma ring: NSIG slots of up to SIGC chunks (one stage)
-  static constexpr int SIG_CHUNK = (BM + BN) * 4;      // sigma_A[128] + sigma_B[128], f32
-  static constexpr int SIG_SLOT = SIGC * SIG_CHUNK;
-  static constexpr int OFF_A = 0;
-  static constexpr int OFF_B = OFF_A + STAGES * STAGE_A;
-  static constexpr int OFF_SFA = OFF_B + STAGES * STAGE_B;
-  static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
-  static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
-  static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;
-  static constexpr int COL_SF0 = NB * BN;              // 384: two 64-column SF buffers after the partials
-  static constexpr int SF_STRIDE = 64;
-  // registers: the launch pool (LAUNCH_REGS x THREADS) re-split by setmaxnreg
-  static constexpr int LAUNCH_REGS = 168, EPI_REGS = 232, CTRL_REGS = 40;
-  static_assert(EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= LAUNCH_REGS * THREADS, "register pool");
-  static_assert(SMEM <= 232448, "shared memory budget");
-  static_assert(COL_SF0 + NSFB * SF_STRIDE <= 512, "TMEM budget");
-};
-
-// Non-blocking phase test (the result is consumed later, so its latency
-// overlaps other work).
-__device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok;
-}
-
-// 32 lanes x 64 columns of one quadrant as two 16x256b.x8 loads: register
-// 32h + 4k + 2s + e holds lane 16h + 8s + t/4, column 8k + 2(t%4) + e
-// (tools/microbench_ldmap.cu).
-__device__ __forceinline__ void tmem_ld_16x256b_x8(uint32_t taddr, float* v) {
-  uint32_t* r = reinterpret_cast<uint32_t*>(v);
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
-      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_ld_part(uint32_t taddr, float* v) {
-  tmem_ld_16x256b_x8(taddr, v);
-  tmem_ld_16x256b_x8(taddr + (16u << 16), v + 32);
-}
-
-__device__ __forceinline__ void mul2v(float& o0, float& o1, float a0, float a1, float b0, float b1) {
-  asm("{\n\t.reg .b64 x, y;\n\tmov.b64 x, {%2, %3};\n\tmov.b64 y, {%4, %5};\n\t"
-      "mul.rn.f32x2 x, x, y;\n\tmov.b64 {%0, %1}, x;\n\t}"
-      : "=f"(o0), "=f"(o1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
-}
-__device__ __forceinline__ void fma2s(float& acc0, float& acc1, float u0, float u1, float s) {
-  asm("{\n\t.reg .b64 w, q, c;\n\tmov.b64 w, {%2, %3};\n\tmov.b64 q, {%4, %4};\n\t"
-      "mov.b64 c, {%0, %1};\n\tfma.rn.f32x2 c, w, q, c;\n\tmov.b64 {%0, %1}, c;\n\t}"
-      : "+f"(acc0), "+f"(acc1)
-      : "f"(u0), "f"(u1), "f"(s));
-}
-
-// acc += sigma_A(row) * (sigma_B(col) * P) for the thread's 4 rows x 16
-// columns.  sig: this chunk's sigma block in shared memory (sigma_A[128] then
-// sigma_B[128]); arow: the thread's first row (quad*32 + t/4); bcol: its
-// first column (grp*64 + 2*(t%4)).
-__device__ __forceinline__ void mbs2_fold(float* acc, const float* p, uint32_t sig, int arow, int bcol) {
-  float sb[16], sa[4];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float2 v = ld_shared_f32x2(sig + (BM + bcol + 8 * k) * 4);
-    sb[2 * k] = v.x;
-    sb[2 * k + 1] = v.y;
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) sa[r] = ld_shared_f32(sig + (arow + 8 * r) * 4);
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const int i = 32 * h + 4 * k + 2 * s;
-        float u0, u1;
-        mul2v(u0, u1, p[i], p[i + 1], sb[2 * k], sb[2 * k + 1]);
-        fma2s(acc[i], acc[i + 1], u0, u1, sa[2 * h + s]);
-      }
-}
-
-// Tile-end store of the thread's 4 rows x 16 columns (pairs at column
-// bcol + 8k), masked to M x N.
-template <bool OUT_BF16>
-__device__ __forceinline__ void mbs2_store(const float* acc, void* c, int64_t ldc, int row0, int col0, int M, int N) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h)
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int row = row0 + 16 * h + 8 * s;
-      if (row >= M) continue;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int i = 32 * h + 4 * k + 2 * s, col = col0 + 8 * k;
-        if constexpr (OUT_BF16) {
-          __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(c) + (int64_t)row * ldc + col;
-          if (col + 1 < N && (ldc % 2) == 0) *reinterpret_cast<uint32_t*>(out) = pack_bf16x2(acc[i], acc[i + 1]);
-          else {
-            if (col < N) out[0] = __float2bfloat16_rn(acc[i]);
-            if (col + 1 < N) out[1] = __float2bfloat16_rn(acc[i + 1]);
-          }
-        } else {
-          float* out = reinterpret_cast<float*>(c) + (int64_t)row * ldc + col;
-          if (col + 1 < N && (ldc % 2) == 0) *reinterpret_cast<float2*>(out) = make_float2(acc[i], acc[i + 1]);
-          else {
-            if (col < N) out[0] = acc[i];
-            if (col + 1 < N) out[1] = acc[i + 1];
-          }
-        }
-      }
-    }
-}
-
-// PAIR: clusters of two CTAs run one cta_group::2 MMA (256 x 128 output
-// tile, M = 256): each CTA holds its own 128 rows of A, half of the B tile
-// (64 rows) and the whole tile's B scale factors; the leader (rank 0) issues
-// the MMAs, its stage barrier collects both CTAs' loads, and both epilogues
-// release a partial buffer on the leader's barrier.  Per SM and 128-K chunk
-// that is 8 KB of A + 4 KB of B + 2 KB of scale factors from L2 instead of
-// 16 KB + 2 KB: the SM's ingress (~50 B/clk, tools/mbs_ab.py knock-outs:
-// multicast does not reduce it) is what bounded the one-SM 128 x 128 form.
-template <bool PAIR, bool OUT_BF16>
-__global__ void __launch_bounds__(Mbs2Cfg<PAIR>::THREADS, 1)
-    k_gemm_mbs2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmSA, const __grid_constant__ CUtensorMap tmSB,
-                const __grid_constant__ Params p) {
-  using C = Mbs2Cfg<PAIR>;
-  constexpr int CL = PAIR ? 2 : 1;
-  constexpr int BN = C::BN, NB = C::NB, STAGES = C::STAGES, EPIW = C::EPIW, NSIG2 = C::NSIG;
-  constexpr int STAGE_B = C::STAGE_B, SFB_BYTES = C::SFB_BYTES, SIG_SLOT = C::SIG_SLOT, SIG_CHUNK = C::SIG_CHUNK;
-  constexpr int OFF_A = C::OFF_A, OFF_B = C::OFF_B, OFF_SFA = C::OFF_SFA, OFF_SFB = C::OFF_SFB;
-  constexpr int OFF_SIG = C::OFF_SIG, OFF_BAR = C::OFF_BAR, COL_SF0 = C::COL_SF0, SF_STRIDE = C::SF_STRIDE;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t a_smem = (smem_u32(smem_raw) + 1023u) & ~1023u;
-  const uint32_t a_full = a_smem + OFF_BAR, a_empty = a_full + 8 * STAGES;
-  const uint32_t a_tfull = a_empty + 8 * STAGES, a_tempty = a_tfull + 8 * NB;
-  const uint32_t a_sfull = a_tempty + 8 * NB, a_sempty = a_sfull + 8 * NSIG2;
-  const uint32_t a_tmem_slot = a_sempty + 8 * NSIG2;
-
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  const int tiles_m = (p.M + BM - 1) / BM, tiles_n = (p.N + BN - 1) / BN;
-  const int groups_m = (tiles_m + CL - 1) / CL;
-  const int num_units = groups_m * tiles_n;
-  const int unit0 = blockIdx.x / CL, unit_step = gridDim.x / CL;
-  uint32_t crank = 0;
-  if constexpr (CL > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
-  const int n_ksteps = (p.K + KSTEP - 1) / KSTEP;
-  const int n_stages = (p.K + KSTAGE - 1) / KSTAGE;
-  const int n_chunks = p.n_chunks, mac_steps = p.mac_steps;
-  const int cps = 4 / mac_steps;  // chunks per 256-K stage (chunks never straddle a stage)
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init_a(a_full + 8 * s, 1);
-      mbar_init_a(a_empty + 8 * s, 1);
-    }
-    for (int b = 0; b < NB; ++b) {
-      mbar_init_a(a_tfull + 8 * b, 1);
-      mbar_init_a(a_tempty + 8 * b, EPIW * CL);
-    }
-    for (int b = 0; b < NSIG2; ++b) {
-      mbar_init_a(a_sfull + 8 * b, 1);
-      mbar_init_a(a_sempty + 8 * b, EPIW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    if constexpr (PAIR) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmSA)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmSB)) : "memory");
-    }
-  }
-  if (warp == C::W_MMA) {
-    if constexpr (PAIR) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(a_tmem_slot) : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(a_tmem_slot) : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if constexpr (CL > 1) cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = ld_shared_u32(a_tmem_slot);
-
-  if (warp >= EPIW) {
-    setmaxnreg_dec<C::CTRL_REGS>();
-    if (warp == C::W_TMA) {
-      // ===================== TMA producer =====================
-      // per 256-K stage: A / B codes, their SF atoms, and (in the sigma ring)
-      // the sigma rows of the stage's chunks
-      uint32_t st = 0, ph = 0, slot = 0, sph = 0, qt = 0;
-      for (int unit = unit0; unit < num_units; unit += unit_step, qt += n_chunks) {
-        const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
-        const int m0 = mb * BM, n0 = nb * BN;
-        // (pair: each CTA loads its A rows, its half of B and both SF blocks;
-        // the leader's barrier expects both CTAs' bytes)
-        constexpr uint32_t SFT = (MXQ_MBS2_EXP & 32) ? 0u : (uint32_t)(SFA_BYTES + SFB_BYTES);
-        const uint32_t tx = PAIR ? 2u * (STAGE_A + STAGE_B + SFT) : (uint32_t)(STAGE_A + STAGE_B + SFT);
-        const uint8_t* sa = p.sfa + (int64_t)mb * p.sfa_kg * ATOM;
-        const uint8_t* sb = p.sfb + (int64_t)nb * p.sfb_kg * ATOM;
-        const float* ga = p.sga + (p.sga_ld ? m0 : 0);
-        const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
-        int sb_bytes = BN * 4;
-        if (p.sgb_ld && p.sgb_ld - n0 < BN) sb_bytes = (int)(p.sgb_ld - n0) * 4;
-        for (int s = 0; s < n_stages; ++s) {
-          const uint32_t fb = a_full + st * 8;
-          trace_at(p, qt + s * cps, 12);
-          mbar_wait_a(a_empty + st * 8, ph ^ 1);
-          trace_at(p, qt + s * cps, 13);
-          if constexpr (PAIR) {
-            const uint32_t fbl = mapa_shared(fb, 0);  // the leader's stage barrier
-            if (crank == 0) expect_tx_e(fb, tx);
-            tma_load_2d_cg2_e(a_smem + OFF_A + st * STAGE_A, &tmA, fbl, s * (KSTAGE / 2), m0);
-            tma_load_2d_cg2_e(a_smem + OFF_B + st * STAGE_B, &tmB, fbl, s * (KSTAGE / 2), n0 + (int)crank * (BN / 2));
-            if (!(MXQ_MBS2_EXP & 32)) {
-              tma_load_2d_cg2_e(a_smem + OFF_SFA + st * SFA_BYTES, &tmSA, fbl, 0, (int)(mb * p.sfa_kg + s * 4));
-              tma_load_2d_cg2_e(a_smem + OFF_SFB + st * SFB_BYTES, &tmSB, fbl, 0, (int)(nb * p.sfb_kg + s * 4));
-            }
-          } else {
-            expect_tx_e(fb, tx);
-            tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, &tmA, fb, s * (KSTAGE / 2), m0);
-            tma_load_2d_e(a_smem + OFF_B + st * STAGE_B, &tmB, fb, s * (KSTAGE / 2), n0);
-            if (!(MXQ_MBS2_EXP & 32)) {
-              bulk_load_e(a_smem + OFF_SFA + st * SFA_BYTES, sa + (int64_t)s * SFA_BYTES, SFA_BYTES, fb);
-              bulk_load_e(a_smem + OFF_SFB + st * SFB_BYTES, sb + (int64_t)s * SFB_BYTES, SFB_BYTES, fb);
-            }
-          }
-          if (++st == STAGES) { st = 0; ph ^= 1; }
-          // the stage's sigma rows (chunks s*cps .. min(+cps, n_chunks)) -> one ring slot
-          const int c0 = s * cps, c1 = min(c0 + cps, n_chunks);
-          if (MXQ_MBS2_EXP & 8) continue;
-          const uint32_t sfb = a_sfull + slot * 8;
-          mbar_wait_a(a_sempty + slot * 8, sph ^ 1);
-          expect_tx_e(sfb, (uint32_t)(c1 - c0) * (BM * 4 + sb_bytes));
-          for (int c = c0; c < c1; ++c) {
-            const uint32_t dst = a_smem + OFF_SIG + slot * SIG_SLOT + (c - c0) * SIG_CHUNK;
-            bulk_load_e(dst, ga + (int64_t)c * p.sga_ld, BM * 4, sfb);
-            bulk_load_e(dst + BM * 4, gb + (int64_t)c * p.sgb_ld, sb_bytes, sfb);
-          }
-          trace_at(p, qt + c0, 11);
-          if (++slot == NSIG2) { slot = 0; sph ^= 1; }
-        }
-      }
-    } else if (warp == C::W_MMA && crank == 0) {
-      // ===================== MMA issuer (the pair's leader) =====================
-      uint32_t g = 0;             // stages consumed (SF buffer parity)
-      uint32_t buf = 0, tph = 0;  // TMEM partial-buffer ring
-      uint32_t st = 0;            // smem ring position
-      uint32_t q = 0;             // chunks issued (trace only)
-      for (int unit = unit0; unit < num_units; unit += unit_step) {
-        int ks = 0;
-        uint64_t adesc = 0, bdesc = 0;
-        uint32_t sfa_col = 0;
-        for (int c = 0; c < n_chunks; ++c, ++q) {
-          const uint32_t dcol = tmem + buf * BN;
-          trace_at(p, q, 0);
-          mbar_wait_a(a_tempty + buf * 8, tph ^ 1u);  // (pair: both CTAs' epilogues)
-          trace_at(p, q, 1);
-          tc_fence_after();
-          int kend = (c + 1) * mac_steps;
-          if (kend > n_ksteps) kend = n_ksteps;
-          const int kbeg = ks;
-          for (; ks < kend; ++ks) {
-            const uint32_t j = (uint32_t)ks & 3u;
-            if (j == 0) {
-              // this stage's SF atoms -> SF buffer g % 2 (the buffer's previous
-              // readers, stage g-2's MMAs, precede these copies in the pipe)
-              sfa_col = tmem + COL_SF0 + (g & (NSFB - 1)) * SF_STRIDE;
-              mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
-              trace_at(p, q, 10);
-              tc_fence_after();
-#pragma unroll
-              for (int jj = 0; jj < 4; ++jj) {
-                if (MXQ_MBS2_EXP & 16) break;
-                if constexpr (PAIR) {  // each CTA's atoms into its own TMEM
-                  sf_cp2_e(sfa_col + 4 * jj, smem_desc(a_smem + OFF_SFA + st * SFA_BYTES + jj * ATOM, 0, 128, 0));
-                  sf_cp2_e(sfa_col + 16 + 4 * jj, smem_desc(a_smem + OFF_SFB + st * SFB_BYTES + jj * ATOM, 0, 128, 0));
-                } else {
-                  sf_cp_e(sfa_col + 4 * jj, a_smem + OFF_SFA + st * SFA_BYTES + jj * ATOM);
-                  sf_cp_e(sfa_col + 16 + 4 * jj, a_smem + OFF_SFB + st * SFB_BYTES + jj * ATOM);
-                }
-              }
-              adesc = operand_desc(a_smem + OFF_A + st * STAGE_A);
-              bdesc = operand_desc(a_smem + OFF_B + st * STAGE_B);
-            }
-            if (!(MXQ_MBS2_EXP & 4)) {
-              if constexpr (PAIR)
-                mma_bs2_e(dcol, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), p.idesc, ks > kbeg ? 1u : 0u,
-                          sfa_col + 4 * j, sfa_col + 16 + 4 * j);
-              else
-                mma_bs_e<false>(dcol, adesc + (uint64_t)(j * 2), bdesc + (uint64_t)(j * 2), p.idesc,
-                                ks > kbeg ? 1u : 0u, sfa_col + 4 * j, sfa_col + 16 + 4 * j);
-            }
-            if (j == 3 || ks + 1 == n_ksteps) {
-              if constexpr (PAIR) tc_commit2_mc_e(a_empty + st * 8, (uint16_t)3);
-              else tc_commit_e(a_empty + st * 8);
-              ++g;
-              if (++st == STAGES) st = 0;
-            }
-          }
-          if constexpr (PAIR) tc_commit2_mc_e(a_tfull + buf * 8, (uint16_t)3);
-          else tc_commit_e(a_tfull + buf * 8);
-          trace_at(p, q, 2);
-          if (++buf == NB) { buf = 0; tph ^= 1; }
-        }
-      }
-    }
-  } else {
-    // ===================== epilogue (warps 0..7) =====================
-    setmaxnreg_inc<C::EPI_REGS>();
-    const int quad = warp & 3, grp = warp >> 2;  // TMEM lane quadrant, 64-column group
-    const uint32_t t_ld = tmem + ((uint32_t)(quad * 32) << 16) + grp * 64;
-    const int arow = quad * 32 + (lane >> 2);          // the thread's rows: arow + 8r
-    const int bcol = grp * 64 + 2 * (lane & 3);        // its columns: bcol + 8k + {0, 1}
-    uint32_t lbuf = 0, ltph = 0, slot = 0, sph = 0;
-    const uint32_t a_tempty_rel = PAIR ? mapa_shared(a_tempty, 0) : a_tempty;  // release on the leader's barrier
-    float acc[64], p0[64], p1[64];
-    uint32_t qe = 0;  // chunks folded (trace only)
-
-    for (int unit = unit0; unit < num_units; unit += unit_step, qe += n_chunks) {
-      const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
-      // chunk 0's partial into p0
-      if (warp == 0) trace_at(p, qe, 3);
-      mbar_wait_a(a_tfull + lbuf * 8, ltph);
-      if (warp == 0) trace_at(p, qe, 4);
-      tc_fence_after();
-      tmem_ld_part(t_ld + lbuf * BN, p0);
-      uint32_t next_ok = 0, sig_ok = 0;  // barrier tests issued one chunk ahead
-      int c = 0, cs = 0;                 // chunk, chunk within its 256-K stage
-      // one chunk: P (loaded into PC) is released, chunk c+1 starts loading
-      // into PN, chunk c is folded
-#define MBS2_TR(k) \
-  if (warp == 0 || warp == 2) trace2_at(p, qe + c, (warp == 2 ? 8 : 0) + (k));
-#define MBS2_STEP(PC, PN)                                                                          \
-  {                                                                                                \
-    tmem_wait_ld();                                                                                \
-    reg_fence<64>(PC);                                                                             \
-    tc_fence_before();                                                                             \
-    __syncwarp();                                                                                  \
-    if constexpr (PAIR) arrive_cluster_e(a_tempty_rel + lbuf * 8);                                 \
-    else arrive_e(a_tempty + lbuf * 8);                                                            \
-    if (warp == 0) trace_at(p, qe + c, 5);                                                         \
-    MBS2_TR(0)                                                                                     \
-    if (++lbuf == NB) { lbuf = 0; ltph ^= 1; }                                                     \
-    if (c + 1 < n_chunks) {                                                                        \
-      if (!next_ok) mbar_wait_a(a_tfull + lbuf * 8, ltph);                                         \
-      MBS2_TR(1)                                                                                   \
-      tc_fence_after();                                                                            \
-      if (!(MXQ_MBS2_EXP & 2)) tmem_ld_part(t_ld + lbuf * BN, PN);                                 \
-    }                                                                                              \
-    MBS2_TR(2)                                                                                     \
-    if (cs == 0 && !sig_ok && !(MXQ_MBS2_EXP & 8)) mbar_wait_a(a_sfull + slot * 8, sph);                                  \
-    if (warp == 0) trace_at(p, qe + c, 6);                                                         \
-    MBS2_TR(3)                                                                                     \
-    {                                                                                              \
-      /* tests for chunk c+2's partial and the next stage's sigma, consumed next step */           \
-      const uint32_t nb2 = lbuf + 1 == NB ? 0 : lbuf + 1, np2 = lbuf + 1 == NB ? ltph ^ 1 : ltph;  \
-      next_ok = c + 2 < n_chunks ? mbar_test(a_tfull + nb2 * 8, np2) : 1u;                         \
-      const uint32_t ns = slot + 1 == NSIG2 ? 0 : slot + 1, nsp = slot + 1 == NSIG2 ? sph ^ 1 : sph; \
-      sig_ok = (cs + 1 == cps || c + 1 == n_chunks) && !(MXQ_MBS2_EXP & 8) ? mbar_test(a_sfull + ns * 8, nsp) : 1u; \
-    }                                                                                              \
-    MBS2_TR(4)                                                                                     \
-    if (!(MXQ_MBS2_EXP & 1)) mbs2_fold(acc, PC, a_smem + OFF_SIG + slot * SIG_SLOT + cs * SIG_CHUNK, arow, bcol); \
-    if (warp == 0) trace_at(p, qe + c, 7);                                                         \
-    MBS2_TR(5)                                                                                     \
-    if (cs + 1 == cps || c + 1 == n_chunks) {                                                      \
-      reg_fence<64>(acc); /* every sigma load has returned (see mbs_body) */                       \
-      __syncwarp();                                                                                \
-      if (!(MXQ_MBS2_EXP & 8)) arrive_e(a_sempty + slot * 8);                                                               \
-      if (++slot == NSIG2) { slot = 0; sph ^= 1; }                                                 \
-      cs = 0;                                                                                      \
-    } else {                                                                                       \
-      ++cs;                                                                                        \
-    }                                                                                              \
-  }
-#pragma unroll 1
-      for (;;) {
-        MBS2_STEP(p0, p1)
-        if (++c == n_chunks) break;
-        MBS2_STEP(p1, p0)
-        if (++c == n_chunks) break;
-      }
-#undef MBS2_STEP
-#undef MBS2_TR
-      mbs2_store<OUT_BF16>(acc, p.c, p.ldc, mb * BM + arow, nb * BN + bcol, p.M, p.N);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if constexpr (CL > 1) cluster_sync();
-  if (warp == C::W_MMA) {
-    tc_fence_after();
-    if constexpr (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-    else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
-  }
-}
-
 template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
 __global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
     k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -1251,72 +793,6 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
     if (TRANS) k_splitk_reduce<OUT_BF16><<<g, 256, 0, st>>>(ws, ksplit, p.N, p.M, p.ws_ld, c, ldc);
     else k_splitk_reduce<OUT_BF16><<<g, 256, 0, st>>>(ws, ksplit, p.M, p.N, p.ws_ld, c, ldc);
   }
-  return check_launch();
-}
-
-template <bool PAIR, bool OUT_BF16>
-static int launch2(const QDesc& a, const QDesc& b, void* c, int64_t ldc, cudaStream_t st) {
-  using C = Mbs2Cfg<PAIR>;
-  constexpr int CL = PAIR ? 2 : 1;
-  auto kern = k_gemm_mbs2<PAIR, OUT_BF16>;
-  static std::atomic<uint64_t> attr_set{0};
-  if (const int rc0 = smem_attr_once(kern, C::SMEM, attr_set)) return rc0;
-  CUtensorMap ta, tb, tsa, tsb;
-  int rc = make_code_map(&ta, a.codes, a.rows, a.cols / 2, a.codes_ld, BM);
-  if (rc) return rc;
-  rc = make_code_map(&tb, b.codes, b.rows, b.cols / 2, b.codes_ld, C::BN / CL);
-  if (rc) return rc;
-  memset(&tsa, 0, sizeof(tsa));
-  memset(&tsb, 0, sizeof(tsb));
-  if constexpr (PAIR) {
-    // scale-factor atoms: rows padded to 256 (two 128-row blocks), sf_kpad / 4 atoms per block
-    rc = make_sf_map(&tsa, a.scales_mma, (a.rows + 255) / 256 * 2 * (a.sf_kpad / 4));
-    if (rc) return rc;
-    rc = make_sf_map(&tsb, b.scales_mma, (b.rows + 255) / 256 * 2 * (b.sf_kpad / 4));
-    if (rc) return rc;
-  }
-  const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
-  const float* ones = ones_buffer();
-  if (!ones) return set_error(ERR_INVALID, "could not allocate the sigma ones row");
-  Params p{};
-  p.sfa = a.scales_mma;
-  p.sfb = b.scales_mma;
-  p.sfa_kg = a.sf_kpad / 4;
-  p.sfb_kg = b.sf_kpad / 4;
-  p.sfb_rb = (int)((b.rows + 255) / 256 * 2);
-  p.sga = ma ? a.sig_t : ones;
-  p.sgb = mbb ? b.sig_t : ones;
-  p.sga_ld = ma ? a.sig_t_ld : 0;
-  p.sgb_ld = mbb ? b.sig_t_ld : 0;
-  p.c = c;
-  p.ldc = ldc;
-  p.M = (int)a.rows;
-  p.N = (int)b.rows;
-  p.K = (int)a.cols;
-  const int macro = ma ? a.macro_size : b.macro_size;
-  p.mac_steps = macro / KSTEP;
-  p.n_chunks = (int)((a.cols + macro - 1) / macro);
-  p.ksplit = 1;
-  p.trace = g_trace;
-  // E2M1 x E2M1, UE8M0 scales, N = 128, M = 128 per CTA (256 for the pair)
-  p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(C::BN >> 3) << 17) | (1u << 23) | ((uint32_t)((BM * CL) >> 4) << 24);
-  const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + C::BN - 1) / C::BN);
-  int clusters = num_sms() / CL;
-  if (units < clusters) clusters = units;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(clusters * CL);
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, tsa, tsb, p);
-  if (e != cudaSuccess) return set_cuda_error(e);
   return check_launch();
 }
 
@@ -1437,9 +913,7 @@ static int launch_shape(const QDesc& ka, const QDesc& kb, void* c, bool bf, int6
   const int tiles_m = (int)((ka.rows + mbs::BM - 1) / mbs::BM), tiles_n = (int)((kb.rows + BN - 1) / BN);
   const int n_stages = (int)((ka.cols + mbs::KSTAGE - 1) / mbs::KSTAGE);
   // one 128-row block: no pairing across M, so no cluster (its second CTA would idle)
-  static int force_cl1 = -1;
-  if (force_cl1 < 0) force_cl1 = getenv("MXQ_MBS_CL1") ? 1 : 0;  // development A/B
-  const int CL = (tiles_m >= 2 && !force_cl1) ? 2 : 1;
+  const int CL = tiles_m >= 2 ? 2 : 1;
   const int macro = (ka.variant == MBS_S || ka.variant == MBS_D) ? ka.macro_size : kb.macro_size;
   int ksplit = choose_ksplit(rows_small, ((tiles_m + CL - 1) / CL) * tiles_n, num_sms() / CL, n_stages, macro);
   // split-K partials: a stream-ordered allocation per call (pool-cached,
@@ -1477,24 +951,7 @@ int launch_gemm_mbs(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_
     if (a.rows <= 32) return launch_shape<32, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
     return launch_shape<64, 4, 4, true>(b, a, c, bf, ldc, (int)a.rows, st);
   }
-  // prefill shapes: 128 x 192 tiles (the experimental 128 x 128 kernel only
-  // with MXQ_MBS_KERNEL=2, development A/B)
-  static int kern2 = -1;
-  if (kern2 < 0) {
-    const char* e = getenv("MXQ_MBS_KERNEL");
-    kern2 = (e && atoi(e) == 2) ? 1 : 0;
-  }
-  if (kern2 && a.rows > 64) {
-    const int tiles_m = (int)((a.rows + mbs::BM - 1) / mbs::BM);
-    if (tiles_m >= 2) return bf ? mbs::launch2<true, true>(a, b, c, ldc, st) : mbs::launch2<true, false>(a, b, c, ldc, st);
-    return bf ? mbs::launch2<false, true>(a, b, c, ldc, st) : mbs::launch2<false, false>(a, b, c, ldc, st);
-  }
-  static int bn_dev = -1;
-  if (bn_dev < 0) {
-    const char* e = getenv("MXQ_MBS_BN");  // development A/B of the tile shape
-    bn_dev = e ? atoi(e) : 0;
-  }
-  if (bn_dev == 128) return launch_shape<128, 3, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
+  // prefill shapes: 128 x 192 tiles, two TMEM partial buffers, 16 epilogue warps
   return launch_shape<192, 2, 16, false>(a, b, c, bf, ldc, (int)a.rows, st);
 }
 

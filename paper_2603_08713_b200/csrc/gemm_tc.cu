@@ -1,24 +1,20 @@
 // gemm_tc.cu -- tcgen05 block-scaled FP4 GEMM for sm_100a (K7 plain MXFP4,
-// K8 MBS, K9 NVFP4).   C[M,N] = A[M,K] . B[N,K]^T
+// K9 NVFP4; the MBS pairs run in gemm_mbs.cu).   C[M,N] = A[M,K] . B[N,K]^T
 //
 // Replaces matmul_quantized (src/gemm.py:137-172).  The reference decodes
 // every element to f32 (g*D/f*s_t) and accumulates f64 products; here the
 // 5th-gen tensor core consumes the packed E2M1 codes and the per-block scale
 // factors directly (kind::mxf4 block32 for OCP32 x OCP32, kind::mxf4nvf4
 // block16 with UE8M0 or UE4M3 scales otherwise) and accumulates in f32 in
-// TMEM.  The MBS factor sigma = 1/(1+m8/256) is per (row, 128-K macro) of each
-// operand, so it cannot ride in the power-of-two block scales: every macro
-// chunk is MMA'd into its own TMEM partial buffer and the epilogue warps fold
-// acc += sigmaA[i,t] * sigmaB[j,t] * P[i,j] in registers (the paper's
-// Appendix E scheme; per-chunk semantics SPEC.md:325).
+// TMEM.
 //
 // Structure (persistent, one CTA per SM, warp-specialised, cta_group::1):
 //   warp 0        TMA producer: A/B code tiles (2-D TMA, 128B swizzle) and the
 //                 scale-factor atoms (1-D bulk copies) into a STAGES-deep ring
 //   warp 1        TMEM allocator + single-thread MMA issuer: tcgen05.cp of the
 //                 scale atoms smem->TMEM, then tcgen05.mma per 64-K step
-//   warps 4..11   epilogue: tcgen05.ld of the accumulator (plain) or of each
-//                 chunk's partial (MBS), sigma / s_t scaling, f32|bf16 stores
+//   16 warps      epilogue: tcgen05.ld of the accumulator, NVFP4 s_t scaling,
+//                 f32|bf16 stores
 //
 // Tile 128 x BN, K stage = 256 elements (128 bytes of codes per row).
 #include <cuda.h>
@@ -39,11 +35,11 @@ constexpr int KSTAGE = 256;            // elements per pipeline stage
 constexpr int KSTEP = 64;              // elements per tcgen05.mma (FP4, K64)
 constexpr int STAGE_BYTES_A = BM * KSTAGE / 2;  // 16 KB
 // Warp roles.  The SM's warp arbiter issues highest-warp-id first, so the
-// latency-critical control warps (TMA producer, MMA issuer, sigma producer)
+// latency-critical control warps (TMA producer, MMA issuer)
 // take the TOP warp ids and the epilogue warps the bottom ones; the epilogue
 // warps' ids stay 4-aligned so warp % 4 is the TMEM lane quadrant they may
 // access.
-constexpr int NUM_CTRL_WARPS = 4;   // TMA producer, MMA issuer, sigma producer, spare
+constexpr int NUM_CTRL_WARPS = 4;   // TMA producer, MMA issuer, two spare
 constexpr int NUM_SFW_WARPS = 4;    // scale-factor writers (one per TMEM lane quadrant)
 
 // ---------------------------------------------------------------------------
@@ -54,26 +50,20 @@ struct Params {
   const uint8_t* sfb;
   int64_t sfa_kg, sfb_kg;  // 4-block groups per 128-row block (sf_kpad / 4)
   int sfb_rb;              // allocated 128-row SF blocks of B
-  const float* sga;     // MBS sigma, transposed (n_macros, ld) f32, or null (sigma = 1)
-  const float* sgb;
-  int64_t sga_ld, sgb_ld;
   const double* tsa;    // NVFP4 tensor scales or null
   const double* tsb;
   void* c;
   int64_t ldc;
   int M, N, K;
-  int macro_steps;      // MBS chunk length in 64-K MMA steps
-  int n_chunks;         // MBS chunks per tile (== n_macros)
   uint32_t idesc;       // instruction descriptor without scale-factor ids
   long long* trace;     // optional clock64 trace of CTA 0 (mxq_debug_set_trace)
-  int dbg;              // ablation flags (MXQ_GEMM_DBG, development only)
 };
 
 
 // Store COLS consecutive bf16 columns (packed pairs) of one row, masked.
 template <int COLS>
 __device__ __forceinline__ void store_row_bf16(const Params& p, int row, int col0, const uint32_t (&pk)[COLS / 2]) {
-  if (row >= p.M || (p.dbg & 4)) return;
+  if (row >= p.M) return;
   __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
   if (col0 + COLS <= p.N && (p.ldc % 8) == 0) {
 #pragma unroll
@@ -93,7 +83,7 @@ __device__ __forceinline__ void store_row_bf16(const Params& p, int row, int col
 // the M x N bounds; 16-byte vector stores when the run is in bounds.
 template <bool OUT_BF16>
 __device__ __forceinline__ void store_row32(const Params& p, int row, int col0, const float (&v)[32]) {
-  if (row >= p.M || (p.dbg & 4)) return;
+  if (row >= p.M) return;
   if constexpr (OUT_BF16) {
     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.c) + (int64_t)row * p.ldc + col0;
     if (col0 + 32 <= p.N && (p.ldc % 8) == 0) {
@@ -125,7 +115,7 @@ __device__ __forceinline__ void store_row32(const Params& p, int row, int col0, 
   }
 }
 
-template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
+template <int BN, int STAGES, int NB, bool SF32, bool OUT_BF16, int CL>
 struct Cfg {
   static constexpr int STAGE_BYTES_B = BN * KSTAGE / 2;
   static constexpr int SF_ATOMS_PER_STAGE = SF32 ? 2 : 4;  // 512-B atoms per 128 rows per stage
@@ -138,11 +128,7 @@ struct Cfg {
   static constexpr int OFF_B = OFF_A + STAGES * STAGE_BYTES_A;
   static constexpr int OFF_SFA = OFF_B + STAGES * STAGE_BYTES_B;
   static constexpr int OFF_SFB = OFF_SFA + STAGES * SFA_BYTES;
-  // MBS sigma ring: NSIG slots of {sigmaA[BM], sigmaB[BN]} f32, one per chunk.
-  static constexpr int NSIG = MBS ? 8 : 0;
-  static constexpr int SIG_SLOT = (BM + BN) * 4;
-  static constexpr int OFF_SIG = OFF_SFB + STAGES * SFB_BYTES;
-  static constexpr int OFF_BAR = OFF_SIG + NSIG * SIG_SLOT;
+  static constexpr int OFF_BAR = OFF_SFB + STAGES * SFB_BYTES;
   // TMEM scale-factor buffers: as many as fit beside the accumulators (<= 4),
   // so the SF writers run up to NSFB-1 stages ahead of the MMAs.
   static constexpr int SF_COLS_STAGE = SF_ATOMS_PER_STAGE * 4 * (1 + NRB);
@@ -155,7 +141,7 @@ struct Cfg {
   // When every smem stage has its own SF buffer, the SF writers reuse the
   // stage's `empty` barrier (MMA completion) instead of a separate commit.
   static constexpr bool SF_ON_EMPTY = (NSFB == STAGES);
-  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * NSIG + 2 * 4;  // + sf_ready[], sf_free[]
+  static constexpr int NUM_BARS = 2 * STAGES + 2 * NB + 2 * 4;  // + sf_ready[], sf_free[]
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + 1024;  // +1024 alignment slack
   static constexpr int TX_BYTES = STAGE_BYTES_A + STAGE_BYTES_B + SFA_BYTES + SFB_BYTES;
   // TMEM columns: NB accumulators of BN columns, then 2 parity sets of SF.
@@ -164,11 +150,11 @@ struct Cfg {
   static constexpr int COL_SF = NB * BN;
   static constexpr int TMEM_COLS_USED = COL_SF + NSFB * SF_STRIDE;
   static constexpr int TMEM_COLS = 512;
-  // 8 epilogue warps: 2 per TMEM lane quadrant, BN/2 columns each.
-  static constexpr int EPIW = MBS ? 8 : 16;  // MBS: 64 columns per thread (issue-bound epilogue)
+  // 16 epilogue warps: 4 per TMEM lane quadrant, BN/4 columns each.
+  static constexpr int EPIW = 16;
   static constexpr int THREADS = (EPIW + NUM_SFW_WARPS + NUM_CTRL_WARPS) * 32;
   static constexpr int W_SFW = EPIW;  // first SF-writer warp (warpgroup aligned)
-  static constexpr int W_TMA = EPIW + 7, W_MMA = EPIW + 6, W_SIG = EPIW + 5;
+  static constexpr int W_TMA = EPIW + 7, W_MMA = EPIW + 6;
 
   static constexpr int COLS = BN / (EPIW / 4);
   static_assert(TMEM_COLS_USED <= 512, "TMEM budget");
@@ -187,19 +173,17 @@ __device__ __forceinline__ void trace_at(const Params& p, int chunk, int slot) {
   }
 }
 
-template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
-__global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::THREADS, 1)
+template <int BN, int STAGES, int NB, bool SF32, bool OUT_BF16, int CL>
+__global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, OUT_BF16, CL>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
-  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
+  using C = Cfg<BN, STAGES, NB, SF32, OUT_BF16, CL>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + NB;
-  uint64_t* sfull = tempty + NB;
-  uint64_t* sempty = sfull + C::NSIG;
-  uint64_t* sf_ready = sempty + C::NSIG;  // [2] SF parity buffer written (4 SF-writer warps)
+  uint64_t* sf_ready = tempty + NB;  // [NSFB] SF buffer written (4 SF-writer warps)
   uint64_t* sf_free = sf_ready + 4;        // [NSFB] SF buffer consumed (MMA commit)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(sf_free + 4);
 
@@ -224,10 +208,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     for (int b = 0; b < NB; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], C::EPIW);
-    }
-    for (int b = 0; b < C::NSIG; ++b) {
-      mbar_init(&sfull[b], 1);
-      mbar_init(&sempty[b], C::EPIW);
     }
     for (int b = 0; b < C::NSFB; ++b) {
       mbar_init(&sf_ready[b], NUM_SFW_WARPS);
@@ -254,7 +234,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
   // division or modulo is left inside them.
   const uint32_t a_full = smem_u32(full), a_empty = smem_u32(empty);
   const uint32_t a_tfull = smem_u32(tfull), a_tempty = smem_u32(tempty);
-  const uint32_t a_sfull = smem_u32(sfull), a_sempty = smem_u32(sempty);
   const uint32_t a_sf_ready = smem_u32(sf_ready), a_sf_free = smem_u32(sf_free);
   const uint32_t a_smem = smem_u32(smem);
 
@@ -273,11 +252,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       for (int s = 0; s < n_stages; ++s) {
         const uint32_t fb = a_full + stage * 8;
         mbar_wait_sleep(a_empty + stage * 8, phase ^ 1);
-        if (p.dbg & 8) {  // experiment: no loads at all
-          arrive_e(fb);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          continue;
-        }
         expect_tx_e(fb, tx);
         tma_load_2d_e(a_smem + C::OFF_A + stage * STAGE_BYTES_A, &tmA, fb, s * (KSTAGE / 2), m0);
         if constexpr (CL == 1) {
@@ -301,7 +275,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const int total = my_units * n_stages;
       uint32_t stage = 0, phase = 0;      // stage g in the smem ring
       uint32_t buf = 0, tphase = 0;       // accumulator ring position
-      const int chunk_len = MBS ? p.macro_steps : (1 << 30);
+      const int chunk_len = 1 << 30;  // one accumulation per tile
       int s = 0, kstep = 0, in_chunk = 0, tchunk = 0;
       bool open = false;
       int unit = unit0;
@@ -390,7 +364,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
       const uint32_t sfa_s = a_smem + C::OFF_SFA + stage * C::SFA_BYTES + lane * 16;
       const uint32_t sfb_s = a_smem + C::OFF_SFB + stage * C::SFB_BYTES + lane * 16;
       const uint32_t col = lane_base + C::COL_SF + par * C::SF_STRIDE;
-      if (!(p.dbg & 16)) {
+      {
         uint32_t r[C::SFA_COLS];
 #pragma unroll
         for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at) {
@@ -399,7 +373,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
         }
         tmem_st<C::SFA_COLS>(col, r);
       }
-      if (!(p.dbg & 16)) {
+      {
         uint32_t r[C::SFB_COLS];
 #pragma unroll
         for (int at = 0; at < C::SF_ATOMS_PER_STAGE; ++at)
@@ -411,34 +385,11 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           }
         tmem_st<C::SFB_COLS>(col + C::SFA_COLS, r);
       }
-      if (!(p.dbg & 16)) tmem_wait_st();
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       arrive_e(a_sf_ready + par * 8);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
-    }
-  } else if (warp == C::W_SIG) {
-    // ===================== sigma producer (MBS) =====================
-    // One slot per chunk: sigmaA[128 rows] and sigmaB[BN cols] as f32 (a
-    // non-MBS operand points at a row of ones with ld 0).
-    if constexpr (MBS) {
-      if (!(p.dbg & 3)) {
-        uint32_t slot = 0, sphase = 0;
-        for (int unit = unit0; unit < num_units; unit += unit_step) {
-          const int m0 = ((unit % groups_m) * CL + (int)crank) * BM, n0 = (unit / groups_m) * BN;
-          const float* ga = p.sga + (p.sga_ld ? m0 : 0);
-          const float* gb = p.sgb + (p.sgb_ld ? n0 : 0);
-          for (int t = 0; t < p.n_chunks; ++t) {
-            const uint32_t fb = a_sfull + slot * 8;
-            mbar_wait_sleep(a_sempty + slot * 8, sphase ^ 1);
-            expect_tx_e(fb, (BM + BN) * 4);
-            const uint32_t dst = a_smem + C::OFF_SIG + slot * C::SIG_SLOT;
-            bulk_load_e(dst, ga + (int64_t)t * p.sga_ld, BM * 4, fb);
-            bulk_load_e(dst + BM * 4, gb + (int64_t)t * p.sgb_ld, BN * 4, fb);
-            if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
-          }
-        }
-      }
     }
   } else if (warp < C::EPIW) {
     // ===================== epilogue =====================
@@ -448,16 +399,15 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
     constexpr int COLS = C::COLS;          // columns per thread
     const int row_in_tile = quad * 32 + lane;
     const uint32_t tmem_lane = tmem + ((uint32_t)(quad * 32) << 16) + half * COLS;
-    uint32_t buf = 0, tphase = 0, slot = 0, sphase = 0;
-    int echunk = 0;
+    uint32_t buf = 0, tphase = 0;
     float scale_nv = 1.0f;
     if (p.tsa && p.tsb) scale_nv = (float)(*p.tsa * *p.tsb);
     for (int unit = unit0; unit < num_units; unit += unit_step) {
       const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
       const int m0 = mb * BM, n0 = nb * BN;
       const int row = m0 + row_in_tile;
-      if (!MBS || (p.dbg & 3)) {
-        // Plain: drain the accumulator 32 columns at a time (scale by the
+      {
+        // Drain the accumulator 16 columns at a time (scale by the
         // NVFP4 tensor scales, convert, store); the TMEM buffer is released
         // right after its last tcgen05.ld.
         mbar_wait_sleep(a_tfull + buf * 8, tphase);
@@ -489,7 +439,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
             __syncwarp();
             if (lane == 0) mbar_arrive_a(a_tempty + buf * 8);
           }
-          if (row < p.M && !(p.dbg & 4)) {
+          if (row < p.M) {
             float* out = reinterpret_cast<float*>(p.c) + (int64_t)row * p.ldc + n0 + half * COLS + c;
             const int col = n0 + half * COLS + c;
             if (col + 16 <= p.N && (p.ldc % 4) == 0) {
@@ -505,63 +455,6 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>::
           }
         }
         if (++buf == NB) { buf = 0; tphase ^= 1; }
-      } else if constexpr (MBS) {
-        float acc[COLS];
-#pragma unroll
-        for (int i = 0; i < COLS; ++i) acc[i] = 0.0f;
-        const uint32_t sig_row = a_smem + C::OFF_SIG + row_in_tile * 4;
-        const uint32_t sig_col = a_smem + C::OFF_SIG + (BM + half * COLS) * 4;
-#pragma unroll 1
-        for (int t = 0; t < p.n_chunks; ++t) {
-          // sigma slot of this chunk (landed long ago) and the partial P.
-          if (lane == 0 && e == 0) trace_at(p, echunk, 2);
-          mbar_wait_a(a_sfull + slot * 8, sphase);
-          const uint32_t sig = sig_col + slot * C::SIG_SLOT;
-          const float sa = ld_shared_f32(sig_row + slot * C::SIG_SLOT);
-          mbar_wait_a(a_tfull + buf * 8, tphase);
-          if (lane == 0 && e == 0) trace_at(p, echunk, 3);
-          if (lane == 0 && e == C::EPIW - 1) trace_at(p, echunk, 7);
-          tc_fence_after();
-#pragma unroll
-          for (int h = 0; h < COLS / 16; ++h) {
-            float v[16];
-            tmem_ld16(tmem_lane + buf * BN + h * 16, v);
-            float4 sb[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) sb[q] = ld_shared_f32x4(sig + (h * 16 + q * 4) * 4);
-            tmem_wait_ld();
-            if (h == COLS / 16 - 1) {
-              // TMEM buffer and sigma slot are free once P is in registers.
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) {
-                mbar_arrive_a(a_tempty + buf * 8);
-                mbar_arrive_a(a_sempty + slot * 8);
-                if (e == 0) trace_at(p, echunk, 6);
-              }
-            }
-            // acc += (sigmaA * sigmaB_j) * P_j   (FMUL2 + FFMA2)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float w0, w1, w2, w3;
-              mul2(w0, w1, sa, sb[q].x, sb[q].y);
-              mul2(w2, w3, sa, sb[q].z, sb[q].w);
-              const int c = h * 16 + q * 4;
-              fma2(acc[c], acc[c + 1], w0, w1, v[q * 4], v[q * 4 + 1]);
-              fma2(acc[c + 2], acc[c + 3], w2, w3, v[q * 4 + 2], v[q * 4 + 3]);
-            }
-          }
-          if (++buf == NB) { buf = 0; tphase ^= 1; }
-          if (++slot == C::NSIG) { slot = 0; sphase ^= 1; }
-          ++echunk;
-        }
-#pragma unroll
-        for (int c = 0; c < COLS; c += 32) {
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = acc[c + i];
-          store_row32<OUT_BF16>(p, row, n0 + half * COLS + c, v);
-        }
       }
     }
   }
@@ -612,21 +505,6 @@ int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t kby
   return 0;
 }
 
-int make_sf_map(CUtensorMap* m, const uint8_t* base, int64_t n_atoms) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return set_error(ERR_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
-  if ((uintptr_t)base % 16) return set_error(ERR_INVALID, "scale-factor atoms must be 16-byte aligned");
-  cuuint64_t dims[2] = {128, (cuuint64_t)n_atoms};
-  cuuint64_t strides[1] = {512};
-  cuuint32_t box[2] = {128, 4};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, (void*)base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return set_error(ERR_INVALID, "cuTensorMapEncodeTiled failed (scale factors)");
-  return 0;
-}
-
 // Block-scaled instruction descriptor (see CUTLASS cute/arch/mma_sm100_desc.hpp
 // InstrDescriptorBlockScaled): a/b format E2M1 = 1 at [7,10)/[10,13), K-major,
 // N>>3 at [17,23), scale format at 23 (1 = UE8M0, 0 = UE4M3), M>>4 at [24,29).
@@ -642,36 +520,12 @@ static uint32_t make_idesc(int n, bool ue8m0) {
 
 long long* g_trace = nullptr;
 
-// Development experiments (MXQ_GEMM_DBG, read once): 1 = switch the MBS
-// accumulator per chunk without the epilogue hand-off, 2 = no switch either.
-// Both change numerics on purpose; 0 (unset) is the product path.
 // TMA-multicast cluster size for the GEMM (MXQ_GEMM_CL=1 disables; dev A/B).
 static int cluster_size() {
   static int v = -1;
   if (v < 0) {
     const char* d = getenv("MXQ_GEMM_CL");
     v = (d && atoi(d) == 1) ? 1 : 2;
-  }
-  return v;
-}
-
-// First-generation MBS kernel (128x128 tiles, N=128 MMAs): the path for
-// macro sizes the 192-column kernel does not take, or forced with
-// MXQ_GEMM_MBS_V1=1 for A/B timing (development).
-static bool mbs_v1() {
-  static int v = -1;
-  if (v < 0) {
-    const char* d = getenv("MXQ_GEMM_MBS_V1");
-    v = (d && atoi(d) == 1) ? 1 : 0;
-  }
-  return v == 1;
-}
-
-static int debug_flags() {
-  static int v = -1;
-  if (v < 0) {
-    const char* d = getenv("MXQ_GEMM_DBG");
-    v = d ? atoi(d) : 0;
   }
   return v;
 }
@@ -693,10 +547,10 @@ const float* ones_buffer() {
   return ptrs[dev];
 }
 
-template <int BN, int STAGES, int NB, bool SF32, bool MBS, bool OUT_BF16, int CL>
+template <int BN, int STAGES, int NB, bool SF32, bool OUT_BF16, int CL>
 static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, bool ue8m0, cudaStream_t st) {
-  using C = Cfg<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
-  auto kern = k_gemm_tc<BN, STAGES, NB, SF32, MBS, OUT_BF16, CL>;
+  using C = Cfg<BN, STAGES, NB, SF32, OUT_BF16, CL>;
+  auto kern = k_gemm_tc<BN, STAGES, NB, SF32, OUT_BF16, CL>;
   static std::atomic<uint64_t> attr_set{0};
   if (const int rc0 = smem_attr_once(kern, C::SMEM, attr_set)) return rc0;
   CUtensorMap ta, tb;
@@ -710,15 +564,6 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.sfa_kg = a.sf_kpad / 4;
   p.sfb_kg = b.sf_kpad / 4;
   p.sfb_rb = (int)((b.rows + 255) / 256 * 2);
-  const bool ma = a.variant == MBS_S || a.variant == MBS_D, mbb = b.variant == MBS_S || b.variant == MBS_D;
-  if constexpr (MBS) {
-    const float* ones = ones_buffer();
-    if (!ones) return set_error(ERR_INVALID, "could not allocate the sigma ones row");
-    p.sga = ma ? a.sig_t : ones;
-    p.sgb = mbb ? b.sig_t : ones;
-    p.sga_ld = ma ? a.sig_t_ld : 0;
-    p.sgb_ld = mbb ? b.sig_t_ld : 0;
-  }
   p.tsa = a.variant == NVFP4 ? a.tensor_scale : nullptr;
   p.tsb = b.variant == NVFP4 ? b.tensor_scale : nullptr;
   p.c = c;
@@ -726,12 +571,8 @@ static int launch_variant(const QDesc& a, const QDesc& b, void* c, int64_t ldc, 
   p.M = (int)a.rows;
   p.N = (int)b.rows;
   p.K = (int)a.cols;
-  const int macro = (a.mant ? a.macro_size : b.macro_size);
-  p.macro_steps = macro / KSTEP;
-  p.n_chunks = (int)((a.cols + macro - 1) / macro);
   p.idesc = make_idesc(BN, ue8m0);
   p.trace = g_trace;
-  p.dbg = debug_flags();
   const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN);
   int clusters = num_sms() / CL;
   if (units < clusters) clusters = units;
@@ -782,12 +623,12 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
     return launch_gemm_mbs(a, b, c, c_dtype, ldc, st);
   }
   if (sf32) {
-    if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, false, true, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, false, true, 2>(a, b, c, ldc, true, st));
-    return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, false, false, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, false, false, 2>(a, b, c, ldc, true, st));
+    if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, true, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, true, 2>(a, b, c, ldc, true, st));
+    return (cluster_size() == 1 ? launch_variant<256, 4, 1, true, false, 1>(a, b, c, ldc, true, st) : launch_variant<256, 4, 1, true, false, 2>(a, b, c, ldc, true, st));
   }
   const bool ue8m0 = !nva;
-  if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, false, false, true, 1>(a, b, c, ldc, ue8m0, st) : launch_variant<256, 4, 1, false, false, true, 2>(a, b, c, ldc, ue8m0, st));
-  return (cluster_size() == 1 ? launch_variant<256, 4, 1, false, false, false, 1>(a, b, c, ldc, ue8m0, st) : launch_variant<256, 4, 1, false, false, false, 2>(a, b, c, ldc, ue8m0, st));
+  if (c_dtype == MXQ_BF16) return (cluster_size() == 1 ? launch_variant<256, 4, 1, false, true, 1>(a, b, c, ldc, ue8m0, st) : launch_variant<256, 4, 1, false, true, 2>(a, b, c, ldc, ue8m0, st));
+  return (cluster_size() == 1 ? launch_variant<256, 4, 1, false, false, 1>(a, b, c, ldc, ue8m0, st) : launch_variant<256, 4, 1, false, false, 2>(a, b, c, ldc, ue8m0, st));
 }
 
 }  // namespace mxq

@@ -239,47 +239,6 @@ __device__ __forceinline__ void mma_bs_e(uint32_t d_tmem, uint64_t adesc, uint64
   }
 }
 
-// ---- cta_group::2 (one MMA over an SM pair, M = 256) ----------------------
-// Address of the same shared-memory object in CTA `rank` of the cluster.
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-// TMA into this CTA's shared memory, completing on a barrier that may live in
-// the peer CTA of the pair (the leader's stage barrier).
-__device__ __forceinline__ void tma_load_2d_cg2_e(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
-                                                  int c1) {
-  asm volatile(MXQ_ELECT
-               "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-               "%3}], [%4];\n\t}" ::"r"(dst),
-               "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_cluster)
-               : "memory");
-}
-__device__ __forceinline__ void arrive_cluster_e(uint32_t bar_cluster) {
-  asm volatile(MXQ_ELECT "mbarrier.arrive.shared::cluster.b64 _, [%0];\n\t}" ::"r"(bar_cluster)
-               : "memory");
-}
-__device__ __forceinline__ void tc_commit2_mc_e(uint32_t bar, uint16_t mask) {
-  asm volatile(MXQ_ELECT
-               "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
-               "%1;\n\t}" ::"r"(bar),
-               "h"(mask)
-               : "memory");
-}
-__device__ __forceinline__ void sf_cp2_e(uint32_t tmem_col, uint64_t desc) {
-  asm volatile(MXQ_ELECT "tcgen05.cp.cta_group::2.32x128b.warpx4 [%0], %1;\n\t}" ::"r"(tmem_col), "l"(desc) : "memory");
-}
-__device__ __forceinline__ void mma_bs2_e(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accum, uint32_t sfa, uint32_t sfb) {
-  asm volatile(
-      "{\n\t.reg .pred p, e_;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e_, 0xffffffff;\n\t"
-      "@e_ tcgen05.mma.cta_group::2.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
-          d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum), "r"(sfa), "r"(sfb)
-      : "memory");
-}
-
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
 // start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48),
 // base offset [49,52), layout [61,64) (2 = 128B swizzle, 0 = none).
@@ -394,9 +353,6 @@ __device__ __forceinline__ void fma2(float& acc0, float& acc1, float w0, float w
 // Host helpers (gemm_tc.cu).
 // 2-D TMA map over packed FP4 codes (inner dim K/2 bytes, box 128 B x box_rows, 128B swizzle).
 int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int64_t kbytes, int64_t ld, int box_rows);
-// 2-D TMA map over a tcgen05 scale-factor atom buffer ([atom][128 x u32]),
-// box = 4 consecutive atoms (one 256-K stage of one 128-row block).
-int make_sf_map(CUtensorMap* m, const uint8_t* base, int64_t n_atoms);
 // 256 f32 ones per device: the sigma row of a non-MBS operand in an MBS GEMM.
 const float* ones_buffer();
 // Development trace buffer (mxq_debug_set_trace), null when off.
