@@ -77,7 +77,10 @@ typedef struct mxq_qtensor {
   int32_t variant;     /* MXQ_OCP32 .. MXQ_NVFP4 */
   int32_t block_size;  /* 32 for OCP32, else 16 */
   int32_t macro_size;  /* MBS macro width (multiple of block_size) */
-  int32_t reserved;
+  int32_t sf_format;   /* GEMM only: 0 = the variant's own scale format in scales_mma (UE8M0, or UE4M3 for
+                          NVFP4); 1 = scales_mma holds the UE8M0 block scales re-expressed as UE4M3 powers of
+                          two (mixed UE8M0 x NVFP4 pairs; the caller folds the power-of-two offset into the
+                          NVFP4 side's tensor_scale) */
   int64_t rows, cols;
   uint8_t* codes;       int64_t codes_ld;   /* bytes between rows, >= cols/2   */
   uint8_t* scales;      int64_t scales_ld;  /* bytes between rows, >= cols/bs  */

@@ -29,7 +29,7 @@ class QT(ctypes.Structure):
 
     _fields_ = [
         ("variant", ctypes.c_int32), ("block_size", ctypes.c_int32),
-        ("macro_size", ctypes.c_int32), ("reserved", ctypes.c_int32),
+        ("macro_size", ctypes.c_int32), ("sf_format", ctypes.c_int32),
         ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
         ("codes", ctypes.c_void_p), ("codes_ld", ctypes.c_int64),
         ("scales", ctypes.c_void_p), ("scales_ld", ctypes.c_int64),

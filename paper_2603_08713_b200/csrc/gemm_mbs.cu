@@ -115,6 +115,8 @@ struct Params {
   int mac_steps;       // macro size / 64 (1, 2 or 4: chunks never straddle a 256-K stage)
   int n_chunks;        // macros per row
   int ksplit;          // K splits (stage-aligned); > 1: f32 partials to ws[split][M][ws_ld]
+  const double* tsa;   // NVFP4 tensor scales (UE4M3 pairs): C *= s_tA s_tB at the store, else null
+  const double* tsb;
   float* ws;
   int64_t ws_ld;
   uint32_t idesc;
@@ -601,12 +603,14 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
       // store the tile row (masked to M x N): the output, or this split's f32 partial
       void* const cout = GROUPED ? gt->g[U.g].c : p.c;
       const int n_out = GROUPED ? gt->g[U.g].n : p.N;
-      if constexpr (GROUPED) {
-        // NVFP4 groups: C = s_tA s_tB (sum of the UE4M3-scaled products), the
-        // plain NVFP4 kernel's epilogue (src/quantize.py:409-423 applies s_t per element)
-        const GroupDesc& G = gt->g[U.g];
-        if (G.tsa) {
-          const float ts = (float)(*G.tsa * *G.tsb);
+      {
+        // NVFP4 / UE4M3 pairs: C = s_tA s_tB (sum of the UE4M3-scaled products),
+        // the plain NVFP4 kernel's epilogue (src/quantize.py:409-423 applies s_t
+        // per element); a side without a tensor scale contributes 1
+        const double* ta = GROUPED ? gt->g[U.g].tsa : p.tsa;
+        const double* tb = GROUPED ? gt->g[U.g].tsb : p.tsb;
+        if (ta || tb) {
+          const float ts = (float)((ta ? *ta : 1.0) * (tb ? *tb : 1.0));
 #pragma unroll
           for (int i = 0; i < COLS; ++i) acc[i] *= ts;
         }
@@ -758,8 +762,12 @@ static int launch(const QDesc& a, const QDesc& b, void* c, int64_t ldc, int kspl
   p.qa = a;
   p.ready = ready;
   p.status = status;
-  // E2M1 x E2M1, UE8M0 scales, N = BN, M = 128 (CUTLASS InstrDescriptorBlockScaled layout)
-  p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | (1u << 23) | ((uint32_t)(BM >> 4) << 24);
+  // E2M1 x E2M1, N = BN, M = 128 (CUTLASS InstrDescriptorBlockScaled layout); scale
+  // format UE8M0 (bit 23) unless the pair carries UE4M3 scales
+  const bool ue4 = a.variant == NVFP4 || a.sf_format == 1;
+  p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((ue4 ? 0u : 1u) << 23) | ((uint32_t)(BM >> 4) << 24);
+  p.tsa = a.variant == NVFP4 ? a.tensor_scale : nullptr;
+  p.tsb = b.variant == NVFP4 ? b.tensor_scale : nullptr;
   const int units = (((p.M + BM - 1) / BM + CL - 1) / CL) * ((p.N + BN - 1) / BN) * ksplit;
   int clusters = num_sms() / CL;
   if (units < clusters) clusters = units;
@@ -891,7 +899,10 @@ static int launch_grouped(const QDesc* ka, const QDesc* kb, void* const* c, int 
 bool gemm_mbs_supported(const QDesc& a, const QDesc& b) {
   const bool ma = a.variant == MBS_S || a.variant == MBS_D, mb = b.variant == MBS_S || b.variant == MBS_D;
   if (!ma && !mb) return false;
-  if (a.variant == NVFP4 || b.variant == NVFP4) return false;  // (an MBS operand makes the SF layout block-16)
+  // one scale format for both operands: UE8M0, or UE4M3 when an NVFP4 side
+  // meets an MBS side whose scales were re-expressed (sf_format 1)
+  const bool ua = a.variant == NVFP4 || a.sf_format == 1, ub = b.variant == NVFP4 || b.sf_format == 1;
+  if (ua != ub) return false;
   const int macro = ma ? a.macro_size : b.macro_size;
   if (ma && mb && a.macro_size != b.macro_size) return false;
   return macro % KSTEP_MBS == 0;

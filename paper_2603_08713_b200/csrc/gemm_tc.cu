@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(Cfg<BN, STAGES, NB, SF32, OUT_BF16, CL>::THREA
     const uint32_t tmem_lane = tmem + ((uint32_t)(quad * 32) << 16) + half * COLS;
     uint32_t buf = 0, tphase = 0;
     float scale_nv = 1.0f;
-    if (p.tsa && p.tsb) scale_nv = (float)(*p.tsa * *p.tsb);
+    if (p.tsa || p.tsb) scale_nv = (float)((p.tsa ? *p.tsa : 1.0) * (p.tsb ? *p.tsb : 1.0));  // (one side: a UE4M3-re-expressed E8M0 operand)
     for (int unit = unit0; unit < num_units; unit += unit_step) {
       const int mb = (unit % groups_m) * CL + (int)crank, nb = unit / groups_m;
       const int m0 = mb * BM, n0 = nb * BN;
@@ -602,7 +602,9 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
   (void)status;
   using namespace tc;
   if (!a.scales_mma || !b.scales_mma) return set_error(ERR_INVALID, "operands need the tcgen05 scale layout");
-  const bool nva = a.variant == NVFP4, nvb = b.variant == NVFP4;
+  // scale format of each operand's SF atoms: UE4M3 for NVFP4 and for UE8M0
+  // scales re-expressed as UE4M3 powers of two (sf_format 1), else UE8M0
+  const bool nva = a.variant == NVFP4 || a.sf_format == 1, nvb = b.variant == NVFP4 || b.sf_format == 1;
   if (nva != nvb) return set_error(ERR_UNSUPPORTED, "UE8M0 x UE4M3 operand pair has no block-scaled MMA form");
   const bool mbs = (a.variant == MBS_S || a.variant == MBS_D || b.variant == MBS_S || b.variant == MBS_D);
   // scale-factor atom layout of each operand: sf_kpad = round_up(K, 256) / sf_block
@@ -610,7 +612,7 @@ int launch_gemm_tc(const QDesc& a, const QDesc& b, void* c, int c_dtype, int64_t
   const bool a32 = a.sf_kpad == kp32 && a.block_size == 32, b32 = b.sf_kpad == kp32 && b.block_size == 32;
   if ((!a32 && a.sf_kpad != kp16) || (!b32 && b.sf_kpad != kp16))
     return set_error(ERR_INVALID, "scale-factor layout does not match a 16- or 32-element block");
-  const bool sf32 = a32 && b32;
+  const bool sf32 = a32 && b32 && !nva;
   if (!sf32 && (a32 || b32)) return set_error(ERR_INVALID, "operands disagree on the scale-factor block");
   if (a.rows > (1 << 30) || b.rows > (1 << 30) || a.cols > (1 << 30)) return set_error(ERR_UNSUPPORTED, "shape too large");
   if (mbs) {

@@ -4,10 +4,12 @@
 for every operand pair the tensor cores can take natively (any two
 E8M0-scaled variants, NVFP4 x NVFP4), applying the MBS factor per 128-K macro
 chunk in the epilogue; its output matches the reference dequantize-then-f64
-matmul within the tolerance stated in DESIGN.md.  ``exact=True`` (and the
-E8M0 x E4M3 pairs, which have no single block-scaled MMA form) use the
-CUDA-core f64 kernel (csrc/gemm_exact.cu), which is bit-identical to the
-reference's ``matmul_quantized`` / ``matmul_reference``.
+matmul within the tolerance stated in DESIGN.md.  E8M0 x NVFP4 pairs
+run on the tensor cores too when the E8M0 operand's block exponents span at
+most 17 (its scales re-expressed exactly as UE4M3 powers of two);
+``exact=True`` (and mixed pairs outside that span) use the CUDA-core f64
+kernel (csrc/gemm_exact.cu), which is bit-identical to the reference's
+``matmul_quantized`` / ``matmul_reference``.
 """
 
 from __future__ import annotations
@@ -91,6 +93,58 @@ def tc_supported(aq: QuantizedTensor, bq: QuantizedTensor) -> bool:
     return True
 
 
+def _e4m3_pow2_code(k: int) -> int:
+    """E4M3 byte of 2**k, k in [-9, 8] (subnormals 2^-9..2^-7 = codes 1, 2, 4)."""
+    return (k + 7) << 3 if k >= -6 else 1 << (k + 9)
+
+
+def _ue4m3_view(q: QuantizedTensor):
+    """The UE8M0 operand's tcgen05 scale atoms re-expressed as UE4M3 powers of
+    two, or None: 2^(b - 127) -> 2^(b - 127 - off) is exact in E4M3 (2^-9 ..
+    2^8) when the block exponents span at most 17 (hard part
+    8, option A; the span the reference measures in within_e4m3_span_fraction,
+    src/metrics.py:185-207).  Returns (scales_mma bytes, off); the power of two
+    2^off is folded into the NVFP4 side's tensor scale.  Cached per tensor."""
+    c = q._cache
+    if "ue4m3" in c:
+        return c["ue4m3"]
+    lo, hi = (int(v) for v in torch.aminmax(q.block_scales))
+    res = None
+    if hi - lo <= 17:
+        off = hi - 127 - 8
+        lut = torch.zeros(256, dtype=torch.uint8)
+        for b in range(lo, hi + 1):
+            lut[b] = _e4m3_pow2_code(b - 127 - off)
+        q.gemm_qt(16)
+        mma = c[("mma", 16)]
+        # (padding bytes hold 0: they map to lut[0], finite, against zero data)
+        res = (lut.to(mma.device)[mma.long()].contiguous(), off)
+    c["ue4m3"] = res
+    return res
+
+
+def _mixed_pair_qts(aq: QuantizedTensor, bq: QuantizedTensor):
+    """Descriptors for a UE8M0 x NVFP4 pair on the tcgen05 path (the UE8M0
+    side's scales re-expressed as UE4M3, its 2^off folded into the NVFP4
+    tensor scale), or None when the span does not fit (exact path)."""
+    if (aq.variant is Variant.NVFP4) == (bq.variant is Variant.NVFP4):
+        return None
+    e8, nv = (aq, bq) if bq.variant is Variant.NVFP4 else (bq, aq)
+    if e8.mbs_mantissas is not None and e8.macro_size % 64:
+        return None
+    view = _ue4m3_view(e8)
+    if view is None:
+        return None
+    sf, off = view
+    q8 = _lib.QT.from_buffer_copy(e8.gemm_qt(16))
+    q8.scales_mma, q8.sf_format = sf.data_ptr(), 1
+    ts = nv._ts_device() * (2.0 ** off)
+    qn = _lib.QT.from_buffer_copy(nv.gemm_qt(16))
+    qn.tensor_scale = ts.data_ptr()
+    keep = (sf, ts)
+    return ((q8, qn) if e8 is aq else (qn, q8)), keep
+
+
 def _sf_block(aq: QuantizedTensor, bq: QuantizedTensor) -> int:
     return 32 if (aq.block_size == 32 and bq.block_size == 32) else 16
 
@@ -115,6 +169,19 @@ def matmul_quantized(aq: QuantizedTensor, bq: QuantizedTensor, cfg: TileConfig =
         _check_out(out, m, n, out_dtype, dev)
     stream = _lib.stream_handle()
     L = _lib.lib()
+    mixed = None if (exact or tc_supported(aq, bq)) else _mixed_pair_qts(aq, bq)
+    if mixed is not None:
+        # UE8M0 x NVFP4 on tensor cores: both scale sets as UE4M3 (exact re-expression)
+        if check:
+            _check_scale_codes(aq)
+            _check_scale_codes(bq)
+        (qa, qb), keep = mixed
+        c = out if out is not None else torch.empty((m, n), dtype=out_dtype, device=dev)
+        dt = _lib.MXQ_BF16 if out_dtype == torch.bfloat16 else _lib.MXQ_F32
+        _lib.check(L.mxq_gemm(ctypes.byref(qa), ctypes.byref(qb), c.data_ptr(), dt, c.stride(0), None, stream),
+                   "matmul_quantized")
+        c._mxq_keep = keep  # the re-expressed scales / folded tensor scale outlive the async launch
+        return c
     if exact or not tc_supported(aq, bq):
         c = torch.empty((m, n), dtype=torch.float32, device=dev)
         status = torch.zeros(4, dtype=torch.int32, device=dev)

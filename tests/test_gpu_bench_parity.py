@@ -119,7 +119,8 @@ def test_criterion_07_all_pairs_on_gpu():
     """C7 on GPU outputs: all 36 variant pairs over 20 random shapes (the
     reference's K choices 16 / 128 / 256 / 384 / 1024, M, N in 1..40).  The
     exact path must be bit-identical to dequantize-then-matmul_reference; the
-    tcgen05 path (every pair tc_supported) within the GEMM tolerance."""
+    default path (tensor cores for all 36 pairs where the scale formats allow)
+    within the GEMM tolerance."""
     rng = np.random.Generator(np.random.PCG64(77))
     k_choices = (16, 128, 256, 384, 1024)
     n_exact = n_tc = 0
@@ -140,13 +141,14 @@ def test_criterion_07_all_pairs_on_gpu():
                 got = M.matmul_quantized(qa[va], qb[vb], exact=True).cpu().numpy()
                 assert np.array_equal(got, want), ("exact", va, vb, m, n, k)
                 n_exact += 1
-                if M.tc_supported(qa[va], qb[vb]):
-                    c = M.matmul_quantized(qa[va], qb[vb]).cpu().numpy()
-                    w64 = da[va].astype(np.float64) @ db[vb].astype(np.float64).T
-                    bound = np.abs(da[va]).astype(np.float64) @ np.abs(db[vb]).astype(np.float64).T
-                    check_tol(c, w64, bound, ("tc", va, vb, m, n, k))
-                    n_tc += 1
-    assert n_exact >= 20 * 25 and n_tc > 0
+                # the default path: tcgen05 for every same-format pair and for
+                # UE8M0 x NVFP4 pairs whose E8M0 span fits UE4M3, else exact
+                c = M.matmul_quantized(qa[va], qb[vb]).cpu().numpy()
+                w64 = da[va].astype(np.float64) @ db[vb].astype(np.float64).T
+                bound = np.abs(da[va]).astype(np.float64) @ np.abs(db[vb]).astype(np.float64).T
+                check_tol(c, w64, bound, ("default", va, vb, m, n, k))
+                n_tc += 1
+    assert n_exact >= 20 * 25 and n_tc == n_exact
 
 
 def test_out_argument_is_validated():

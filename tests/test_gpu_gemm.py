@@ -69,15 +69,36 @@ def test_tc_gemm_llama_shape_mbs_h():
     _check(c, want, bound, "llama")
 
 
-def test_mixed_scale_types_route_to_exact():
+@pytest.mark.parametrize("va,vb", [("mbs_d", "nvfp4"), ("nvfp4", "ocp32"), ("mx16_oas", "nvfp4"), ("nvfp4", "mbs_s")])
+def test_mixed_scale_types(va, vb):
+    """UE8M0 x NVFP4 pairs (/root/reference/pkg/tests/test_gemm.py:73-80): on
+    the tensor cores when the UE8M0 operand's exponents span <= 17 (scales
+    re-expressed exactly as UE4M3 powers of two, 2^off folded into s_t) --
+    within the GEMM tolerance; exact=True stays bit-identical to the
+    reference; a wide exponent span falls back to the exact kernel."""
     rng = np.random.Generator(np.random.PCG64(9))
-    a = rng.standard_normal((40, 256)).astype(np.float32)
-    b = rng.standard_normal((24, 256)).astype(np.float32)
-    aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_D))
+    for (m, n, k) in [(40, 24, 256), (300, 640, 2048), (130, 384, 2880)]:
+        if "ocp32" in (va, vb) and k % 32:
+            continue
+        a = rng.standard_t(4, (m, k)).astype(np.float32)
+        b = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+        aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant(va)))
+        bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant(vb)))
+        assert not M.tc_supported(aq, bq)
+        c = M.matmul_quantized(aq, bq).cpu().numpy()
+        want, bound = _ref(a, b, va, vb)
+        _check(c, want, bound, (va, vb, m, n, k))
+        ex = M.matmul_quantized(aq, bq, exact=True).cpu().numpy()
+        assert np.array_equal(ex, O.matmul_quantized(O.quantize(a, va), O.quantize(b, vb)))
+        cb = M.matmul_quantized(aq, bq, out_dtype=torch.bfloat16).float().cpu().numpy()
+        assert np.array_equal(cb, torch.from_numpy(c).to(torch.bfloat16).float().numpy())
+    # exponent span > 17 (block maxima from 1e-6 to 1e3): the exact kernel
+    a = rng.standard_normal((64, 256)).astype(np.float32) * np.logspace(-6, 3, 64, dtype=np.float32)[:, None]
+    b = rng.standard_normal((32, 256)).astype(np.float32)
+    aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MX16_OAS))
     bq = M.quantize_tensor(b, M.SchemeConfig(M.Variant.NVFP4))
-    assert not M.tc_supported(aq, bq)
     c = M.matmul_quantized(aq, bq).cpu().numpy()
-    assert np.array_equal(c, O.matmul_quantized(O.quantize(a, "mbs_d"), O.quantize(b, "nvfp4")))
+    assert np.array_equal(c, O.matmul_quantized(O.quantize(a, "mx16_oas"), O.quantize(b, "nvfp4")))
 
 
 def test_tk_validation_like_reference():
