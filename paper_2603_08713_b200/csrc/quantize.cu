@@ -959,17 +959,20 @@ int launch_quantize(const void* x, int dtype, int64_t x_ld, const QDesc& q, int 
       g.macro = q.macro_size;
       g.G = macro_lanes(q.macro_size);
       g.nmac = (cols + q.macro_size - 1) / q.macro_size;
-      if (g.G > 32) return set_error(ERR_UNSUPPORTED, "macro_size > 512 is not supported by the CUDA quantizer");
       const int64_t ngroups = rows * g.nmac;
-      if (q.variant == MBS_S && g.G * 16 == g.macro) {
-        switch (g.G) {  // power-of-two macro of G units
+      if (q.variant == MBS_S && g.G * 16 == g.macro && g.G <= 128) {
+        switch (g.G) {  // power-of-two macro of G units (runs of 4 units: up to 32 lanes per macro, 2048 elements)
           case 1: RUN_LAUNCH(SQ_MBS_S, 1); break;
           case 2: RUN_LAUNCH(SQ_MBS_S, 2); break;
           case 4: RUN_LAUNCH(SQ_MBS_S, 4); break;
           case 8: RUN_LAUNCH(SQ_MBS_S, 8); break;
           case 16: RUN_LAUNCH(SQ_MBS_S, 16); break;
-          default: RUN_LAUNCH(SQ_MBS_S, 32); break;
+          case 32: RUN_LAUNCH(SQ_MBS_S, 32); break;
+          case 64: RUN_LAUNCH(SQ_MBS_S, 64); break;
+          default: RUN_LAUNCH(SQ_MBS_S, 128); break;
         }
+      } else if (g.G > 32) {
+        return set_error(ERR_UNSUPPORTED, "this macro_size is not supported by the CUDA quantizer (MBS-S: powers of two up to 2048; otherwise up to 512)");
       } else if (q.variant == MBS_S) {
         const FastDiv fd = make_fastdiv((uint32_t)g.nmac);
         const int grid = grid_for(ngroups * g.G, 256);

@@ -252,13 +252,14 @@ def test_nvfp4_rounding_boundaries_match_oracle():
 def test_streaming_quantizer_ragged_rows_match_oracle(variant):
     """Row-tiled streaming kernels: rows longer than one 4096-element tile and
     not a multiple of it, tiny (f32-subnormal) and huge blocks in one row
-    (the MBS-S folded / unfolded scaling paths), macro 64 and 256 for MBS-S."""
+    (the MBS-S folded / unfolded scaling paths), MBS-S macros 32 .. 2048
+    (runs of four units: one thread, a lane pair, .. 32 lanes per macro)."""
     rng = np.random.Generator(np.random.PCG64(77))
     t = rng.standard_t(4, (5, 4096 + 1024 + 96)).astype(np.float32)
     t[1, :256] *= np.float32(1e-40)
     t[2, 512:640] *= np.float32(1e30)
     t[3, 1000:1100] = 0.0
-    macros = (64, 128, 256) if variant == "mbs_s" else (128,)
+    macros = (32, 64, 128, 256, 512, 1024, 2048) if variant == "mbs_s" else (128,)
     for mac in macros:
         if variant == "ocp32" and t.shape[1] % 32:
             continue
@@ -286,3 +287,22 @@ def test_strided_bf16_views_quantize_like_contiguous(variant):
         qa = M.quantize_tensor(v, cfg)
         qb = M.quantize_tensor(v.contiguous(), cfg)
         assert qa == qb, (variant, v.stride(), v.data_ptr() % 32)
+
+
+def test_mbs_macro_1024_gemm_on_tensor_cores():
+    """macro_size 1024 (beyond the reference's swept set, allowed by
+    src/quantize.py:163-166): MBS-S quantization bit-exact, and the MBS
+    GEMM (chunks spanning four 256-K stages) within the GEMM tolerance."""
+    rng = np.random.Generator(np.random.PCG64(5))
+    a = rng.standard_t(4, (300, 3072)).astype(np.float32)
+    b = (rng.standard_normal((520, 3072)) * 0.02).astype(np.float32)
+    qa = M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S, macro_size=1024))
+    qb = M.quantize_tensor(b, M.SchemeConfig(M.Variant.MBS_S, macro_size=1024))
+    oa, ob = O.quantize(a, "mbs_s", macro_size=1024), O.quantize(b, "mbs_s", macro_size=1024)
+    assert np.array_equal(_np(qa.codes), oa.codes) and np.array_equal(_np(qa.mbs_mantissas), oa.mbs_mantissas)
+    assert M.tc_supported(qa, qb)
+    c = M.matmul_quantized(qa, qb, M.TileConfig(t_k=1024)).cpu().numpy().astype(np.float64)
+    da, db = O.dequantize(oa).astype(np.float64), O.dequantize(ob).astype(np.float64)
+    want, bound = da @ db.T, np.abs(da) @ np.abs(db).T
+    assert np.linalg.norm(c - want) / np.linalg.norm(want) <= 1e-5
+    assert np.all(np.abs(c - want) <= 2.0 ** -16 * bound)
