@@ -584,8 +584,9 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
         ++q;
       };
       int c = U.c_lo;
+      constexpr bool UNROLL8 = true;
 #pragma unroll 1
-      while (c < U.c_hi && (q & (NSIG - 1))) { chunk_step(std::integral_constant<int, -1>{}); ++c; }
+      while (c < U.c_hi && (!UNROLL8 || (q & (NSIG - 1)))) { chunk_step(std::integral_constant<int, -1>{}); ++c; }
 #pragma unroll 1
       for (; c + NSIG <= U.c_hi; c += NSIG) {
         static_assert(NSIG == 8, "the aligned block below is written for eight sigma slots");

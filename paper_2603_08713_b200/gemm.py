@@ -288,22 +288,24 @@ def matmul_quantized_grouped(aqs, bqs, cfg: TileConfig = TileConfig(), *, out_dt
 
 def quantize_matmul(a, bq: QuantizedTensor, cfg: SchemeConfig = SchemeConfig(Variant.MBS_S),
                     tile: TileConfig = TileConfig(), *, out_dtype: torch.dtype = torch.float32,
-                    out: torch.Tensor = None, check: bool = True):
+                    out: torch.Tensor = None, check: bool = True, fused: bool = False):
     """``(matmul_quantized(aq, bq), aq)`` with ``aq = quantize_tensor(a, cfg)``
     (src/quantize.py:709-725, src/gemm.py:137-172) -- the activation side of
     a quantized linear layer.
 
-    For an MBS-S activation (bf16, more than 64 rows) against an MBS / E8M0
-    weight, the quantization runs inside the GEMM launch (csrc/gemm_mbs.cu,
-    ``fused_quant_a``): each CTA quantizes its share of A's 128-row blocks and
-    the GEMM consumes a block as soon as it is published, so there is no
-    separate quantizer launch.  Every other case makes the two calls.  The
-    result and ``aq`` are bit-identical either way.
+    By default the two calls run back to back (quantizer launch + GEMM
+    launch).  ``fused=True`` (an MBS-S bf16 activation of more than 64 rows
+    against an MBS / E8M0 weight) runs the quantization inside the GEMM
+    launch instead (csrc/gemm_mbs.cu ``fused_quant_a``: the running CTAs
+    claim 8-row slices of A, quantize them with the standalone kernel's
+    arithmetic and publish them before the first tile loads) -- one launch,
+    no co-residency assumption, but measured slower than the two launches
+    (DESIGN.md section 7).  The result and ``aq`` are bit-identical either way.
     """
     from . import quantize as _q
 
     cfg = cfg if isinstance(cfg, SchemeConfig) else SchemeConfig(cfg)
-    fusable = (cfg.variant is Variant.MBS_S and bq.variant in (Variant.MBS_S, Variant.MBS_D, Variant.MX16,
+    fusable = (fused and cfg.variant is Variant.MBS_S and bq.variant in (Variant.MBS_S, Variant.MBS_D, Variant.MX16,
                                                                 Variant.MX16_OAS, Variant.OCP32)
                and isinstance(a, torch.Tensor) and a.dtype == torch.bfloat16 and a.is_cuda
                # the pair must be one the tcgen05 MBS kernel takes (else: two calls,

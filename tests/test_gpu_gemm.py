@@ -204,7 +204,7 @@ def test_quantize_matmul_fused_matches_two_step(m, n, k, macro, wv, out_dtype):
     wq = M.quantize_tensor(w, wcfg)
     acfg = M.SchemeConfig(M.Variant.MBS_S, macro_size=macro)
     tile = M.TileConfig(t_k=max(macro, 128))
-    c_f, aq_f = M.quantize_matmul(a, wq, acfg, tile, out_dtype=out_dtype)
+    c_f, aq_f = M.quantize_matmul(a, wq, acfg, tile, out_dtype=out_dtype, fused=True)
     aq_2 = M.quantize_tensor(a, acfg)
     c_2 = M.matmul_quantized(aq_2, wq, tile, out_dtype=out_dtype)
     torch.cuda.synchronize()
@@ -223,12 +223,12 @@ def test_quantize_matmul_fused_repeated_and_nonfinite():
     ref = [M.matmul_quantized(M.quantize_tensor(x, M.SchemeConfig(M.Variant.MBS_S)), wq) for x in xs]
     for _ in range(2):
         for x, r in zip(xs, ref):
-            c, _ = M.quantize_matmul(x, wq)
+            c, _ = M.quantize_matmul(x, wq, fused=True)
             assert torch.equal(c, r)
     bad = xs[0].clone()
     bad[300, 7] = float("nan")
     with pytest.raises(ValueError):
-        M.quantize_matmul(bad, wq)
+        M.quantize_matmul(bad, wq, fused=True)
 
 
 # ---------------------------------------------------------------------------
@@ -285,7 +285,7 @@ def test_quantize_matmul_fused_not_co_resident():
         "a = torch.randn(1024, 2048, device='cuda', generator=g).to(torch.bfloat16)\n"
         "w = (torch.randn(2304, 2048, device='cuda', generator=g) * 0.02).to(torch.bfloat16)\n"
         "wq = M.quantize_tensor(w, M.SchemeConfig(M.Variant.MBS_D))\n"
-        "c, aq = M.quantize_matmul(a, wq)\n"
+        "c, aq = M.quantize_matmul(a, wq, fused=True)\n"
         "c2 = M.matmul_quantized(M.quantize_tensor(a, M.SchemeConfig(M.Variant.MBS_S)), wq)\n"
         "torch.cuda.synchronize()\n"
         "assert torch.equal(c, c2)\n"
