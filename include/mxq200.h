@@ -108,7 +108,8 @@ void mxq_debug_set_trace(long long* dev_buf);
  * mbs_mode must be 0 (exact SSE search, src/quantize.py:438-461); the lut
  * mode has its own entry point below.  cand/n_cand: HOST array of candidate bytes
  * (CandidateSet.mantissas); augment_static as SchemeConfig.augment_static.
- * scratch: device u32[4] (scratch[0] status bits, scratch[1] NVFP4 amax).
+ * scratch: device u32[4] (scratch[0] status bits, scratch[1] NVFP4 amax); the call
+ * zeroes the four words before its kernels run.
  */
 int mxq_quantize(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor* q, int32_t mbs_mode,
                  const uint8_t* cand, int32_t n_cand, int32_t augment_static, uint32_t* scratch, void* stream);

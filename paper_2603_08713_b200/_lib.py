@@ -115,15 +115,32 @@ def check(rc: int, what: str) -> None:
     raise RuntimeError(f"{what}: {msg}")
 
 
+_device_ok = False
+_devices: dict = {}
+
+
 def require_device() -> torch.device:
-    """The CUDA device the product path runs on (fails loudly without one)."""
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2603_08713_b200 needs a CUDA B200; no CUDA device is visible")
-    lib()
-    return torch.device("cuda", torch.cuda.current_device())
+    """The CUDA device the product path runs on (fails loudly without one).
+    The availability check and the library load run once per process."""
+    global _device_ok
+    if not _device_ok:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2603_08713_b200 needs a CUDA B200; no CUDA device is visible")
+        lib()
+        _device_ok = True
+    idx = torch.cuda.current_device()
+    d = _devices.get(idx)
+    if d is None:
+        d = _devices[idx] = torch.device("cuda", idx)
+    return d
 
 
 def stream_handle() -> int:
+    """cudaStream_t of the current stream (torch's internal accessor: the
+    public torch.cuda.current_stream() costs ~10 us of Python per call)."""
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 

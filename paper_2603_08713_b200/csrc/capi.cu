@@ -103,6 +103,10 @@ int mxq_quantize(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qtensor
   if (((uintptr_t)x % al) || ((x_ld * esz) % al))
     return set_error(ERR_UNSUPPORTED, "input must be aligned with a row pitch of 32 bytes (bf16) / 16 bytes (f32)");
   if (!q->scales && !q->scales_mma) return set_error(ERR_INVALID, "no scale output buffer");
+  {  // the call's status words start at zero (the kernels only OR error bits in)
+    const cudaError_t e = cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), (cudaStream_t)stream);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
   const bool mbs = q->variant == MBS_S || q->variant == MBS_D;
   if (mbs && !q->mant && !q->sig_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
   if (q->scales_mma) {  // padding atoms must hold finite scale codes
@@ -131,6 +135,10 @@ int mxq_quantize_mbs_lut(const void* x, int32_t x_dtype, int64_t x_ld, const mxq
   if (x_ld < q->cols || ((uintptr_t)x % 16) || ((x_ld * esz) % 16))
     return set_error(ERR_UNSUPPORTED, "input must be 16-byte aligned with a 16-byte row pitch");
   if (!q->mant && !q->sig_t) return set_error(ERR_INVALID, "MBS quantize needs a mantissa buffer");
+  {
+    const cudaError_t e = cudaMemsetAsync(scratch, 0, 4 * sizeof(uint32_t), (cudaStream_t)stream);
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
   if (q->scales_mma) {
     const int64_t rows_pad = (q->rows + 255) / 256 * 256;
     if (rows_pad != q->rows || q->sf_kpad != q->cols / q->block_size) {
@@ -197,6 +205,10 @@ int mxq_quantize_gemm(const void* x, int32_t x_dtype, int64_t x_ld, const mxq_qt
   if (!x || !scratch) return set_error(ERR_INVALID, "null input or scratch");
   if (x_ld < a->cols) return set_error(ERR_INVALID, "x_ld < cols");
   cudaStream_t st = (cudaStream_t)stream;
+  {
+    const cudaError_t e = cudaMemsetAsync(scratch, 0, 2 * sizeof(uint32_t), st);  // (words 2-3: launch_gemm_mbs_fused)
+    if (e != cudaSuccess) return set_cuda_error(e);
+  }
   const int64_t rows_pad = (a->rows + 255) / 256 * 256;
   if (rows_pad != a->rows || a->sf_kpad != a->cols / a->block_size) {  // padding atoms must hold finite codes
     cudaError_t e = cudaMemsetAsync(a->scales_mma, 0, (size_t)(rows_pad * a->sf_kpad), st);

@@ -167,7 +167,9 @@ class QuantizedTensor:
         object.__setattr__(self, "variant", Variant(self.variant))
         object.__setattr__(self, "shape", tuple(int(s) for s in self.shape))
         for f in ("codes", "block_scales", "e4m3_scales", "mbs_mantissas"):
-            object.__setattr__(self, f, _to_device_u8(getattr(self, f), dev))
+            a = getattr(self, f)
+            if not (a is None or (isinstance(a, torch.Tensor) and a.dtype == torch.uint8 and a.device == dev)):
+                object.__setattr__(self, f, _to_device_u8(a, dev))
         object.__setattr__(self, "_cache", {})
 
     # ---- reference accessors ------------------------------------------------
@@ -455,23 +457,38 @@ def _as_device_2d(t, bs: int):
 
 
 class _Outputs:
-    """Device buffers one quantize call writes."""
+    """Device buffers one quantize call writes, carved out of ONE allocation
+    (16-byte aligned views): codes, row-major scales, tcgen05 scale atoms,
+    mantissas, transposed sigma, the NVFP4 tensor scale and the 4-word status
+    (zeroed by the C call itself)."""
 
     def __init__(self, variant: Variant, rows: int, cols: int, bs: int, macro: int, dev, gemm_layout: bool):
-        self.codes_buf = torch.empty((rows, _round_up(cols // 2, 16)), dtype=torch.uint8, device=dev)
-        self.codes = self.codes_buf[:, : cols // 2]
-        self.scales = torch.empty((rows, cols // bs), dtype=torch.uint8, device=dev)
-        self.rows_pad = _round_up(rows, 256)
-        self.kpad = _round_up(cols, 256) // bs
-        self.sf_mma = (torch.empty(self.rows_pad * self.kpad, dtype=torch.uint8, device=dev)
-                       if gemm_layout else None)
         mbs = variant in MBS_VARIANTS
         nmac = -(-cols // macro)
-        self.mant = torch.empty((rows, nmac), dtype=torch.uint8, device=dev) if mbs else None
-        self.sig_t = (torch.empty((nmac, self.rows_pad), dtype=torch.float32, device=dev)
-                       if (mbs and gemm_layout) else None)
-        self.ts = torch.empty(1, dtype=torch.float64, device=dev) if variant is Variant.NVFP4 else None
-        self.status = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.rows_pad = _round_up(rows, 256)
+        self.kpad = _round_up(cols, 256) // bs
+        pitch = _round_up(cols // 2, 16)
+        sizes = [("codes", rows * pitch), ("scales", rows * (cols // bs)),
+                 ("sf", self.rows_pad * self.kpad if gemm_layout else 0),
+                 ("mant", rows * nmac if mbs else 0),
+                 ("sig", 4 * nmac * self.rows_pad if (mbs and gemm_layout) else 0),
+                 ("ts", 8 if variant is Variant.NVFP4 else 0), ("status", 16)]
+        offs, total = {}, 0
+        for name, n in sizes:
+            offs[name] = total
+            total += _round_up(n, 16)
+        buf = torch.empty(total, dtype=torch.uint8, device=dev)
+        part = lambda name, n: buf[offs[name]:offs[name] + n]
+        self.keep = buf
+        self.codes_buf = part("codes", rows * pitch).view(rows, pitch)
+        self.codes = self.codes_buf[:, : cols // 2]
+        self.scales = part("scales", rows * (cols // bs)).view(rows, cols // bs)
+        self.sf_mma = part("sf", self.rows_pad * self.kpad) if gemm_layout else None
+        self.mant = part("mant", rows * nmac).view(rows, nmac) if mbs else None
+        self.sig_t = (part("sig", 4 * nmac * self.rows_pad).view(torch.float32).view(nmac, self.rows_pad)
+                      if (mbs and gemm_layout) else None)
+        self.ts = part("ts", 8).view(torch.float64) if variant is Variant.NVFP4 else None
+        self.status = part("status", 16).view(torch.int32)
 
     def qt(self, variant: Variant, rows: int, cols: int, bs: int, macro: int) -> _lib.QT:
         q = _lib.QT()
@@ -488,6 +505,18 @@ class _Outputs:
         if self.ts is not None:
             q.tensor_scale = self.ts.data_ptr()
         return q
+
+
+_CAND_CACHE: dict = {}
+
+
+def _cand_array(candidates) -> np.ndarray:
+    """Candidate bytes as a uint8 host array, built once per candidate set."""
+    key = tuple(candidates.mantissas)
+    arr = _CAND_CACHE.get(key)
+    if arr is None:
+        arr = _CAND_CACHE[key] = np.asarray(key, dtype=np.uint8)
+    return arr
 
 
 def quantize_tensor(t, cfg: SchemeConfig, *, check: bool = True, gemm_layout: bool = True) -> QuantizedTensor:
@@ -512,7 +541,7 @@ def quantize_tensor(t, cfg: SchemeConfig, *, check: bool = True, gemm_layout: bo
     q = out.qt(cfg.variant, rows, cols, bs, macro)
     stream = _lib.stream_handle()
     L = _lib.lib()
-    cand = np.asarray(cfg.candidates.mantissas, dtype=np.uint8)
+    cand = _cand_array(cfg.candidates)
     if cfg.variant is Variant.MBS_D and cfg.mbs_mode == "lut":
         lut = np.ascontiguousarray(build_error_lut(cfg.candidates).entries, dtype=np.float32)
         rc = L.mxq_quantize_mbs_lut(x.data_ptr(), dt, x.stride(0), ctypes.byref(q), cand.ctypes.data, len(cand),
@@ -541,7 +570,7 @@ def _result(out: "_Outputs", variant: Variant, rows: int, cols: int, bs: int, ma
         block_scales=None if nv else out.scales, e4m3_scales=out.scales if nv else None,
         mbs_mantissas=out.mant, tensor_scale=ts)
     c = res._cache
-    c["keep"] = out.codes_buf
+    c["keep"] = out.keep
     c["status"] = out.status
     if out.sf_mma is not None:
         c[("mma", bs)] = out.sf_mma
