@@ -701,7 +701,7 @@ __device__ __forceinline__ double pw_sum_smem_t(const double* base, int64_t s, i
   }
 }
 
-__device__ double pw_sum_smem(const double* base, int64_t s, int64_t n) { return pw_sum_smem_t<3>(base, s, n); }
+__device__ __noinline__ double pw_sum_smem(const double* base, int64_t s, int64_t n) { return pw_sum_smem_t<3>(base, s, n); }
 
 // MBS-D candidate bytes and (LUT mode) the error table (src/quantize.py:482-504:
 // [regime][candidate][bin] fp16 values widened to f32, exact), passed BY VALUE
@@ -722,6 +722,13 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
                                                                  uint32_t* __restrict__ status,
                                                                  const __grid_constant__ MbsdTables tab) {
   __shared__ double s_sq[MBSD_THREADS * MBSD_STRIDE];
+  // the LUT in shared memory: a dynamically indexed kernel parameter would be
+  // copied to local memory per thread
+  __shared__ float s_lut[LUT ? 2 * 16 * 64 : 1];
+  if constexpr (LUT) {
+    for (int i = threadIdx.x; i < 2 * 16 * 64; i += MBSD_THREADS) s_lut[i] = (&tab.lut[0][0][0])[i];
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int sub = lane & (g.G - 1);
   double* gbase = s_sq + (threadIdx.x - sub) * MBSD_STRIDE;  // this group's slots
@@ -765,22 +772,32 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
       const uint32_t biased = e8m0_biased_16(a, true);
       const float sf = exp2i_f32(127 - (int)biased);
       if constexpr (LUT) {
-        const double sf64 = ldexp(1.0, 127 - (int)biased);
+        // bin of v = |x| * SF (src/quantize.py:507-542): floor(v * 64) below 1,
+        // floor((v - 1) * 64 / 7) above.  v is exact in f32 wherever a bin can
+        // be nonzero (an f32 x times a power of two; an f32-subnormal v is
+        // below 2^-126 and lands in bin 0 either way), v - 1 and the products
+        // by 64 and 7 are exact, and floor(RN64(t / 7)) == floor(t / 7) (t has
+        // a 24-bit significand, so t / 7 is never within an f64 half-ulp of
+        // an integer from below) -- the reference's f64 division per element
+        // becomes an f32 estimate with an exact integer correction.
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const double x64 = (double)v[i];
-          const double vv = __dmul_rn(fabs(x64), sf64);
-          double tv;
-          if (vv < 1.0) {
-            long long b = (long long)__dmul_rn(vv, 64.0);
-            b = b < 0 ? 0 : (b > 63 ? 63 : b);
-            tv = (double)tab.lut[0][t][b];
+          const float vf = fabsf(v[i]) * sf;
+          float tv;
+          if (vf < 1.0f) {
+            int b = (int)(vf * 64.0f);
+            b = b > 63 ? 63 : b;
+            tv = s_lut[(0 * 16 + t) * 64 + b];
           } else {
-            long long b = (long long)__ddiv_rn(__dmul_rn(__dsub_rn(vv, 1.0), 64.0), 7.0);
+            const float tt = (vf - 1.0f) * 64.0f;
+            int b = (int)(tt * 0.142857142857142857f);
+            if (7.0f * (float)(b + 1) <= tt) ++b;
+            else if (7.0f * (float)b > tt) --b;
             b = b < 0 ? 0 : (b > 63 ? 63 : b);
-            tv = (double)tab.lut[1][t][b];
+            tv = s_lut[(1 * 16 + t) * 64 + b];
           }
-          mine[i] = active ? __dmul_rn(__dmul_rn(x64, x64), tv) : 0.0;
+          const double x64 = (double)v[i];
+          mine[i] = active ? __dmul_rn(__dmul_rn(x64, x64), (double)tv) : 0.0;
         }
       } else {
         const bool fast = biased >= 4 && biased <= 250;
@@ -810,7 +827,22 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
       }
       __syncwarp();
       double sse = 0.0;
-      if (sub == 0 && live_group) sse = pw_sum_smem(gbase, 0, width);
+      if (g.G == 8) {
+        // full 128-element macros: numpy's eight strided accumulators, one per
+        // lane of the group (r_j = sq[j] + sq[j+8] + ... in ascending order),
+        // then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles -- the same
+        // operations in the same order as pw_leaf, 16 dependent adds per lane
+        // instead of 128 by one lane
+        double r = sq_at(gbase, sub);
+#pragma unroll
+        for (int k = 1; k < 16; ++k) r = __dadd_rn(r, sq_at(gbase, sub + 8 * k));
+        r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));  // r0+r1, r2+r3, ...
+        r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 2));  // (r0+r1)+(r2+r3), ...
+        r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 4));  // the macro's sum at sub 0
+        if (sub == 0 && live_group) sse = width == 128 ? r : pw_sum_smem(gbase, 0, width);
+      } else if (sub == 0 && live_group) {
+        sse = pw_sum_smem(gbase, 0, width);
+      }
       __syncwarp();
       if (sub == 0) {
         const bool better = (t == 0) || (sse < best_sse) || (sse == best_sse && m8 < best_m8);
