@@ -124,11 +124,22 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   __shared__ unsigned long long s_cnt[2];
   __shared__ Range s_stack[64];
   __shared__ Frame s_frames[64];
+  __shared__ float2 s_uv[256];  // (RN(1/f), RN(1.5/f)) per mantissa byte (see k_dequantize)
+  for (int i = threadIdx.x; i < 256; i += QS_THREADS) {
+    const float f = mbs_factor((uint32_t)i);
+    s_uv[i] = make_float2(__fdiv_rn(1.0f, f), __fdiv_rn(1.5f, f));
+  }
   const int64_t n = rows * cols;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Range node = node_at(n, depth, blockIdx.x);
+  // A node of 128 * 2^k elements is a perfect tree of consecutive 128-element
+  // leaves (numpy's split halves it exactly at every level): its leaves are
+  // implicit.  Only irregular nodes are enumerated (serially, by thread 0 --
+  // that walk was the CTA's critical path: 22 % barrier stalls).
+  const bool implicit = node.n >= 128 && (node.n & 127) == 0 && (((node.n >> 7) & ((node.n >> 7) - 1)) == 0) &&
+                        (node.n >> 7) <= QS_MAXLEAF;
   if (threadIdx.x == 0) {
-    s_nl = enum_leaves(node, s_leaf, s_stack);
+    s_nl = implicit ? (int)(node.n >> 7) : enum_leaves(node, s_leaf, s_stack);
     s_cnt[0] = s_cnt[1] = 0ull;
   }
   __syncthreads();
@@ -146,6 +157,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   const uint32_t ucols = (uint32_t)cols;
   const int bs_shift = has_q ? (q.block_size == 32 ? 5 : 4) : 4;
   const uint32_t umacro = has_q && q.mant ? (uint32_t)q.macro_size : 1u;
+  const bool ref_vec = dtype == DT_BF16 && (ref_ld % 4) == 0 && ((uintptr_t)ref % 8) == 0;
   // Two leaves per warp iteration: their element loads overlap, and the two
   // leaves' numpy-order accumulator chains run side by side (lanes 0-15 on
   // leaf t = 0, lanes 16-31 on t = 1) -- the chains, not the loads, bound
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
     for (int t = 0; t < 2; ++t) {
       const int lj = li + t * QS_WARPS;
       if (lj >= nl) break;
-      const Range lf = s_leaf[lj];
+      const Range lf = implicit ? Range{node.s + 128 * (int64_t)lj, 128} : s_leaf[lj];
       const int64_t row0 = lf.s / cols;
       const uint32_t c0 = (uint32_t)(lf.s - row0 * cols);
       // A lane's 4 elements (p0..p0+3) lie in one row and one 16-block: leaves
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
         uint32_t codes4 = 0x1111u;  // (dense recon: no flush statistics)
         if (has_q) {
           const uint8_t* cp = q.codes + r * q.codes_ld + (c >> 1);
-          codes4 = (uint32_t)cp[0] | ((uint32_t)cp[1] << 8);
+          codes4 = (uint32_t)*reinterpret_cast<const uint16_t*>(cp);  // (c is a multiple of 4: 2-byte aligned)
           const uint32_t sc = q.scales[r * q.scales_ld + (c >> bs_shift)];
           if (q.variant == NVFP4) {
             bad |= ((sc & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
@@ -188,9 +200,9 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
               // two (see k_dequantize)
               float u = 1.0f, v = 1.5f;
               if (q.mant) {
-                const float f = mbs_factor(m8);
-                u = __fdiv_rn(1.0f, f);
-                v = __fdiv_rn(1.5f, f);
+                const float2 uv = s_uv[m8];
+                u = uv.x;
+                v = uv.y;
               }
   #pragma unroll
               for (int j = 0; j < 4; ++j) {
@@ -212,9 +224,20 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   #pragma unroll
           for (int j = 0; j < 4; ++j) xv[j] = recon[r * recon_ld + c + j];
         }
+        float rv4[4];
+        if (ref_vec) {  // four bf16 (8 bytes) in one load
+          const uint2 w = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(ref) + r * ref_ld + c);
+          rv4[0] = __uint_as_float(w.x << 16);
+          rv4[1] = __uint_as_float(w.x & 0xFFFF0000u);
+          rv4[2] = __uint_as_float(w.y << 16);
+          rv4[3] = __uint_as_float(w.y & 0xFFFF0000u);
+        } else {
+  #pragma unroll
+          for (int j = 0; j < 4; ++j) rv4[j] = load_ref(ref, dtype, r * ref_ld + c + j);
+        }
   #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const float rv = load_ref(ref, dtype, r * ref_ld + c + j);
+          const float rv = rv4[j];
           const double r64 = (double)rv;
           const double d = __dsub_rn(r64, (double)xv[j]);
           a4[j] = __dmul_rn(r64, r64);
@@ -237,7 +260,7 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
     double acc = 0.0;
     if (lj < nl) {
       const double* v = s_sq[warp][t][(lane >> 3) & 1];
-      const int j = lane & 7, ln = (int)s_leaf[lj].n;
+      const int j = lane & 7, ln = implicit ? 128 : (int)s_leaf[lj].n;
       acc = v[j];
       for (int i = 8; i < ln; i += 8) acc = __dadd_rn(acc, v[i + j]);
     }
