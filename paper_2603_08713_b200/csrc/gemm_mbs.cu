@@ -390,6 +390,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
       // nothing and keeps the 32-register producer loop free of spills)
       if constexpr (FUSED) wait_ready(p.ready, (uint32_t)((p.M + FQ_ROWS - 1) / FQ_ROWS));
       uint32_t st = 0, ph = 0, slot = 0, sph = 0;
+      uint32_t tq = 0, tsq = 0;  // (trace only)
       for (int unit = unit0; unit < num_units; unit += unit_step) {
         const Unit U = unit_of(unit);
         const int m0 = U.mb * BM, n0 = U.nb * BN;
@@ -423,7 +424,9 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           // its 32 registers)
           const CUtensorMap* mA = GROUPED ? &gt->g[U.g].tmA : tmA;
           const CUtensorMap* mB = GROUPED ? &gt->g[U.g].tmB : tmB;
+          trace_at(p, tsq, 13);
           mbar_wait_a(a_empty + st * 8, ph ^ 1);
+          trace_at(p, tsq++, 14);
           expect_tx_e(fb, tx);
           tma_load_2d_e(a_smem + OFF_A + st * STAGE_A, mA, fb, s * (KSTAGE / 2), m0);
           if constexpr (CL == 1) {
@@ -440,7 +443,9 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
           // sigma slices of the chunks that start in this stage
           while (chunk < U.c_hi && chunk * mac_steps < 4 * (s + 1)) {
             const uint32_t sfb = a_sfull + slot * 8;
+            trace_at(p, tq, 11);
             mbar_wait_a(a_sempty + slot * 8, sph ^ 1);
+            trace_at(p, tq++, 12);
             expect_tx_e(sfb, BM * 4 + sb_bytes);
             const uint32_t dst = a_smem + OFF_SIG + slot * SIG_SLOT;
             bulk_load_e(dst, ga + (int64_t)chunk * p.sga_ld, BM * 4, sfb);
@@ -483,6 +488,7 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
 #ifndef MXQ_NO_SFFREE
               if (g >= NSFB) mbar_wait_a(a_sffree + (g & (NSFB - 1)) * 8, ((g / NSFB) - 1) & 1u);
 #endif
+              trace_at(p, q, 15);
               mbar_wait_a(a_full + st * 8, (g / STAGES) & 1u);
               trace_at(p, q, 10);
               tc_fence_after();
@@ -848,7 +854,7 @@ static int launch_grouped(const QDesc* ka, const QDesc* kb, void* const* c, int 
       p.n_chunks = 1;
     }
     p.ksplit = 1;
-    p.trace = nullptr;
+    p.trace = g_trace;
     // E2M1 x E2M1, N = BN, M = 128; scale format UE8M0 (bit 23) or UE4M3 (NVFP4)
     p.idesc = (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) | ((nv ? 0u : 1u) << 23) | ((uint32_t)(BM >> 4) << 24);
     t->n_groups = ng;

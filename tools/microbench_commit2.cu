@@ -48,6 +48,7 @@ __global__ void k(int iters, int cmode, long long* out) {
   const int do_wait = (cmode >> 8) & 1;       // try_wait on an already-complete barrier after each commit
   const int do_fence = (cmode >> 9) & 1;      // tcgen05.fence::after_thread_sync after each commit
   const int multi_bar = (cmode >> 10) & 1;    // rotate over 4 commit barriers
+  const int rot_d = (cmode >> 11) & 1;        // rotate the accumulator over 4 N-column buffers per commit group
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tbase;
   __shared__ __align__(8) uint64_t fin;
@@ -107,7 +108,7 @@ __global__ void k(int iters, int cmode, long long* out) {
     for (int i = 0; i < iters; i += 4) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        mma<KIND, CG>(tmem, ad + j * 2, bd + j * 2, idesc, tmem + 256, tmem + 320);
+        mma<KIND, CG>(tmem + (rot_d ? (uint32_t)((nc & 3) * N) : 0u), ad + j * 2, bd + j * 2, idesc, tmem + 256, tmem + 320);
         if (commit_every && ++cnt == commit_every) {
           cnt = 0;
           const uint32_t cba = (uint32_t)__cvta_generic_to_shared(&cb[multi_bar ? (nc & 3) : 0]);
@@ -171,6 +172,19 @@ void run(int iters, int sf_rot = 0) {
 }
 
 int main() {
+  // decode tiles (16 / 32 / 64 columns): per-chunk commits into rotating buffers
+  run<4, 16, 1>(2048, 0);
+  run<4, 16, 1>(2048, 2);
+  run<4, 16, 1>(2048, 2 | 1024);
+  run<4, 16, 1>(2048, 2 | 1024 | 2048);
+  run<4, 16, 1>(2048, 4 | 1024 | 2048);
+  run<4, 16, 1>(2048, 1 | 1024 | 2048);
+  run<5, 16, 1>(2048, 0);
+  run<5, 16, 1>(2048, 4);
+  run<4, 32, 1>(2048, 0);
+  run<4, 32, 1>(2048, 2 | 1024 | 2048);
+  run<4, 64, 1>(2048, 0);
+  run<4, 64, 1>(2048, 2 | 1024 | 2048);
   run<4, 256, 1>(2048, 0);
   run<4, 256, 1>(2048, 1);
   run<4, 256, 1>(2048, 2);
