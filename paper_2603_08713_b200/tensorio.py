@@ -10,10 +10,18 @@ reference writes load here bit-exactly (tests/test_tensorio.py).
 B200 side: all sections of a file are staged through ONE pinned host buffer
 with asynchronous copies on the caller's stream and a single synchronisation,
 so a save is one D2H of exactly the payload bytes and a load is one file read
-plus one H2D per section.  The tcgen05 scale-factor layout is not stored (the
-format is the reference's); ``load_quant`` leaves it to be rebuilt on the
-device on first GEMM use (``mxq_build_gemm_layout``), or eagerly with
-``gemm_layout=True``.
+plus one H2D per section.
+
+The tcgen05 operand layout (scale-factor atoms of 128 rows x 4 blocks, and
+the transposed f32 sigma^T of MBS tensors) is exported to a SIDECAR file,
+``<path>.mxg`` (magic ``MXG1``, same envelope), never into the MXQ1 file, so
+MXQ1 stays byte-identical to the reference's.  ``save_quant(...,
+gemm_layout=True)`` writes both; ``load_quant`` uploads a sidecar that
+matches the container (shape, variant, sizes and the CRC-32 of the MXQ1
+payload) straight into the operand cache, so serving skips the on-device
+rebuild (``mxq_build_gemm_layout``); without a sidecar the layout is rebuilt
+on first GEMM use, or eagerly with ``gemm_layout=True``.  A sidecar that does
+not match its container raises ``ValueError`` (stale export).
 
 Header validation and error messages follow the reference line by line
 (src/tensorio.py:64-74, :87-120, :152-215), as pure-host functions
@@ -26,17 +34,22 @@ import json
 import os
 import struct
 import tempfile
+import zlib
 from typing import Optional
 
 import numpy as np
 
 __all__ = [
-    "TENSOR_MAGIC", "QUANT_MAGIC", "save_tensor", "load_tensor", "save_quant", "load_quant",
-    "parse_quant_header", "read_quant_host", "quant_section_sizes",
+    "TENSOR_MAGIC", "QUANT_MAGIC", "LAYOUT_MAGIC", "save_tensor", "load_tensor", "save_quant", "load_quant",
+    "save_gemm_layout", "parse_quant_header", "parse_layout_header", "read_quant_host", "quant_section_sizes",
+    "layout_path",
 ]
 
 TENSOR_MAGIC = b"MXT1"
 QUANT_MAGIC = b"MXQ1"
+LAYOUT_MAGIC = b"MXG1"
+LAYOUT_NAME = "tcgen05-sf-atom-128x4"  # csrc/layout.cu: 128-row x 4-block atoms, 512 B, rows padded to 256
+LAYOUT_VERSION = 1
 _MBS = ("mbs_s", "mbs_d")
 _VARIANTS = ("ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4")  # Variant values, src/quantize.py:70-76
 
@@ -161,6 +174,60 @@ def read_quant_host(path: str) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# MXG1 sidecar: the tcgen05 operand layout (host logic)
+# ---------------------------------------------------------------------------
+def layout_path(path: str) -> str:
+    """Sidecar path of an MXQ1 container."""
+    return path + ".mxg"
+
+
+def _layout_geometry(f: dict, sf_block: int) -> tuple[int, int]:
+    """(rows_pad, kpad) of the SF-atom layout for `sf_block` (quantize.py
+    gemm_qt): rows padded to 256, K padded to 256 elements."""
+    rows_pad = -(-f["rows"] // 256) * 256
+    return rows_pad, (-(-f["cols"] // 256) * 256) // sf_block
+
+
+def layout_sections(f: dict, sf_blocks) -> list[tuple[str, int]]:
+    """(name, bytes) of an MXG1 payload, in file order: one SF-atom array per
+    scale block size, then sigma^T (n_macros x rows_pad f32) for MBS."""
+    out = []
+    for sb in sf_blocks:
+        rows_pad, kpad = _layout_geometry(f, sb)
+        out.append((f"sf{sb}", rows_pad * kpad))
+    if f["has_mbs"]:
+        rows_pad, _ = _layout_geometry(f, 16)
+        out.append(("sig_t", -(-f["cols"] // f["macro_size"]) * rows_pad * 4))
+    return out
+
+
+def parse_layout_header(header: dict, f: dict, crc: Optional[int], path: str = "<mxg1>") -> list[tuple[str, int]]:
+    """Validate an MXG1 header against its container's normalised MXQ1 fields
+    `f` (and the MXQ1 payload's CRC-32 when given); returns the sections."""
+    try:
+        name = header["layout"]
+        version = int(header["version"])
+        fields = {k: header[k] for k in ("variant", "block_size", "macro_size")}
+        shape = [int(d) for d in header["shape"]]
+        sf_blocks = [int(b) for b in header["sf_blocks"]]
+        hcrc = int(header["mxq1_crc32"])
+    except (KeyError, ValueError, TypeError) as exc:
+        raise ValueError(f"{path}: malformed layout header: {exc}") from exc
+    if name != LAYOUT_NAME or version != LAYOUT_VERSION:
+        raise ValueError(f"{path}: unsupported layout {name!r} v{version}")
+    if (shape != [f["rows"], f["cols"]] or fields["variant"] != f["variant"]
+            or int(fields["block_size"]) != f["block_size"] or int(fields["macro_size"]) != f["macro_size"]):
+        raise ValueError(f"{path}: layout does not match its container (stale export)")
+    if not sf_blocks or any(b not in (16, 32) for b in sf_blocks) or len(set(sf_blocks)) != len(sf_blocks):
+        raise ValueError(f"{path}: invalid sf_blocks {sf_blocks}")
+    if 32 in sf_blocks and f["block_size"] != 32:
+        raise ValueError(f"{path}: 32-element SF atoms need an OCP32 container")
+    if crc is not None and hcrc != crc:
+        raise ValueError(f"{path}: layout does not match its container (payload CRC-32 differs: stale export)")
+    return layout_sections(f, sf_blocks)
+
+
+# ---------------------------------------------------------------------------
 # Device paths
 # ---------------------------------------------------------------------------
 def _pinned(nbytes: int):
@@ -168,10 +235,12 @@ def _pinned(nbytes: int):
     return torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)[:nbytes]
 
 
-def save_quant(q, path: str) -> None:
+def save_quant(q, path: str, gemm_layout: bool = False) -> None:
     """Write a QuantizedTensor (CUDA buffers) as an MXQ1 container, atomically
     (src/tensorio.py:125-149).  One pinned staging buffer, one D2H per
-    section on the current stream, one synchronisation."""
+    section on the current stream, one synchronisation.  ``gemm_layout=True``
+    also exports the tcgen05 operand layout to the ``.mxg`` sidecar; without
+    it, a sidecar left from an earlier save of `path` is removed."""
     import torch
     rows, cols = q.shape
     has_mbs = q.mbs_mantissas is not None
@@ -193,14 +262,87 @@ def save_quant(q, path: str) -> None:
         buf[off:off + 8].numpy()[:] = np.frombuffer(struct.pack("<d", float(q.tensor_scale)), dtype=np.uint8)
     hb = _header_bytes(header)
     _atomic_write_parts(path, (QUANT_MAGIC, struct.pack("<I", len(hb)), hb, memoryview(buf.numpy())))
+    if gemm_layout:
+        save_gemm_layout(q, path, crc=zlib.crc32(memoryview(buf.numpy())))
+    elif os.path.exists(layout_path(path)):
+        os.unlink(layout_path(path))  # (it described the container just replaced)
+
+
+def save_gemm_layout(q, path: str, sf_blocks=None, crc: Optional[int] = None) -> str:
+    """Export `q`'s tcgen05 operand layout (built on the device if it is not
+    cached yet) to the MXG1 sidecar of the MXQ1 container at `path`, which
+    must already hold `q` (its payload CRC-32 binds the two).  `sf_blocks`:
+    the SF-atom block sizes to store (default: the tensor's own; OCP32 may
+    add 16 for pairs with block-16 partners).  Returns the sidecar path."""
+    import torch
+    if crc is None:
+        fh, _, _ = _open_quant(path)  # (positioned at the payload)
+        with fh:
+            crc = zlib.crc32(fh.read())
+    rows, cols = q.shape
+    sf_blocks = list(sf_blocks) if sf_blocks else [int(q.block_size)]
+    f = {"variant": q.variant.value, "rows": rows, "cols": cols, "block_size": int(q.block_size),
+         "macro_size": int(q.macro_size), "has_mbs": q.mbs_mantissas is not None}
+    secs = layout_sections(f, sf_blocks)
+    header = {"layout": LAYOUT_NAME, "version": LAYOUT_VERSION, "variant": f["variant"], "shape": [rows, cols],
+              "block_size": f["block_size"], "macro_size": f["macro_size"], "sf_blocks": sf_blocks,
+              "mxq1_crc32": int(crc)}
+    parse_layout_header(header, f, crc)  # (self-check)
+    srcs = []
+    for sb in sf_blocks:
+        q.gemm_qt(sb)
+        srcs.append(q._cache[("mma", sb)])
+    if f["has_mbs"]:
+        srcs.append(q._cache["sig_t"])
+    buf = _pinned(sum(n for _, n in secs))
+    off = 0
+    for t, (_, n) in zip(srcs, secs):
+        assert t.numel() * t.element_size() == n
+        buf[off:off + n].copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+        off += n
+    torch.cuda.current_stream().synchronize()
+    hb = _header_bytes(header)
+    out = layout_path(path)
+    _atomic_write_parts(out, (LAYOUT_MAGIC, struct.pack("<I", len(hb)), hb, memoryview(buf.numpy())))
+    return out
+
+
+def _load_layout(q, path: str, f: dict, crc: int, dev) -> bool:
+    """Upload a matching MXG1 sidecar into q's operand cache; False when
+    there is none.  Raises ValueError for a sidecar that does not match."""
+    import torch
+    lp = layout_path(path)
+    if not os.path.exists(lp):
+        return False
+    with open(lp, "rb") as fh:
+        header, plen = _read_header(fh, lp, LAYOUT_MAGIC)
+        secs = parse_layout_header(header, f, crc, lp)
+        total = sum(n for _, n in secs)
+        if plen != total:
+            raise ValueError(f"{lp}: payload length {plen} != expected {total}")
+        buf = _pinned(total)
+        if fh.readinto(memoryview(buf.numpy())) != total:
+            raise ValueError(f"{lp}: payload length mismatch while reading")
+    off = 0
+    for name, n in secs:
+        t = buf[off:off + n].to(dev, non_blocking=True)
+        off += n
+        if name == "sig_t":
+            rows_pad, _ = _layout_geometry(f, 16)
+            q._cache["sig_t"] = t.view(torch.float32).view(-1, rows_pad)
+        else:
+            q._cache[("mma", int(name[2:]))] = t
+    q._cache["staging_mxg"] = buf
+    return True
 
 
 def load_quant(path: str, device=None, gemm_layout: bool = False):
     """Read an MXQ1 container into a QuantizedTensor in CUDA memory,
     bit-exactly (src/tensorio.py:152-215; same ValueErrors).  The payload is
     read straight into a pinned buffer and copied to the device section by
-    section.  ``gemm_layout=True`` also builds the tcgen05 operand layouts
-    now instead of on first GEMM use."""
+    section.  A matching ``.mxg`` sidecar is uploaded as the tcgen05 operand
+    layout (no rebuild); ``gemm_layout=True`` builds whatever the sidecar did
+    not provide now instead of on first GEMM use."""
     import torch
     from . import _lib
     from .quantize import QuantizedTensor, Variant
@@ -222,10 +364,13 @@ def load_quant(path: str, device=None, gemm_layout: bool = False):
                         macro_size=f["macro_size"], codes=codes, block_scales=None if nv else scales,
                         e4m3_scales=scales if nv else None, mbs_mantissas=mant, tensor_scale=ts)
     q._cache["staging"] = buf  # keep the pinned source alive until the copies ran
+    if os.path.exists(layout_path(path)):
+        _load_layout(q, path, f, zlib.crc32(memoryview(buf.numpy())), dev)
     if gemm_layout:
         q.gemm_qt()
     torch.cuda.current_stream().synchronize()
     q._cache.pop("staging", None)
+    q._cache.pop("staging_mxg", None)
     return q
 
 

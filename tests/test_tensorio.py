@@ -11,6 +11,7 @@ equals the device quantization and feeds the tcgen05 GEMM.
 
 import json
 import os
+import shutil
 import struct
 
 import numpy as np
@@ -194,3 +195,83 @@ def test_gpu_loaded_weights_feed_the_gemm(tmp_path):
             c0 = M.matmul_quantized(aq, wq)
             c1 = M.matmul_quantized(aq, wl)
             assert torch.equal(c0, c1), (va, vw, eager)
+
+
+# ---------------------------------------------------------------------------
+# MXG1 sidecar (tcgen05 operand layout export)
+# ---------------------------------------------------------------------------
+def _layout_header(**kw):
+    h = {"layout": tio.LAYOUT_NAME, "version": tio.LAYOUT_VERSION, "variant": "mbs_d", "shape": [300, 2880],
+         "block_size": 16, "macro_size": 128, "sf_blocks": [16], "mxq1_crc32": 1234}
+    h.update(kw)
+    return h
+
+
+_F = {"variant": "mbs_d", "rows": 300, "cols": 2880, "block_size": 16, "macro_size": 128, "has_mbs": True,
+      "has_tensor_scale": False}
+
+
+def test_layout_header_sections():
+    secs = tio.parse_layout_header(_layout_header(), _F, 1234)
+    # SF atoms: rows padded to 256 (512), K padded to 256 elements (3072) / 16; sigma^T: 23 macros x 512 f32
+    assert secs == [("sf16", 512 * 192), ("sig_t", 23 * 512 * 4)]
+    f32 = dict(_F, variant="ocp32", block_size=32, macro_size=32, has_mbs=False)
+    secs = tio.parse_layout_header(_layout_header(variant="ocp32", block_size=32, macro_size=32, sf_blocks=[32, 16]),
+                                   f32, None)
+    assert secs == [("sf32", 512 * 96), ("sf16", 512 * 192)]
+
+
+@pytest.mark.parametrize("kw, msg", [
+    ({"shape": [301, 2880]}, "stale export"),
+    ({"variant": "mbs_s"}, "stale export"),
+    ({"macro_size": 256}, "stale export"),
+    ({"mxq1_crc32": 99}, "CRC-32"),
+    ({"version": 2}, "unsupported layout"),
+    ({"layout": "other"}, "unsupported layout"),
+    ({"sf_blocks": [32]}, "OCP32 container"),
+    ({"sf_blocks": [16, 16]}, "invalid sf_blocks"),
+    ({"sf_blocks": "x"}, "malformed layout header"),
+])
+def test_layout_header_rejects(kw, msg):
+    with pytest.raises(ValueError, match=msg):
+        tio.parse_layout_header(_layout_header(**kw), _F, 1234)
+
+
+@pytest.mark.gpu
+def test_gpu_layout_sidecar_round_trip(tmp_path):
+    """save_quant(gemm_layout=True) exports the SF atoms (and sigma^T) next to
+    a byte-unchanged MXQ1 file; load_quant uploads them without a rebuild,
+    bit-identical to a fresh build, and the GEMM on the loaded weights equals
+    the in-memory one.  A sidecar left over from another tensor is refused."""
+    import torch
+    import paper_2603_08713_b200 as M
+    g = torch.Generator(device="cuda").manual_seed(9)
+    w = torch.randn(300, 2880, device="cuda", generator=g) * 0.02
+    a = torch.randn(64, 2880, device="cuda", generator=g)
+    for va, vw in (("mbs_s", "mbs_d"), ("nvfp4", "nvfp4"), ("ocp32", "ocp32"), ("mx16_oas", "mx16_oas")):
+        wq = M.quantize_tensor(w, M.SchemeConfig(M.Variant(vw)))
+        p0, p1 = str(tmp_path / f"{vw}.plain.mxq"), str(tmp_path / f"{vw}.mxq")
+        tio.save_quant(wq, p0)
+        tio.save_quant(wq, p1, gemm_layout=True)
+        assert open(p0, "rb").read() == open(p1, "rb").read()  # the container is unchanged
+        assert os.path.exists(tio.layout_path(p1)) and not os.path.exists(tio.layout_path(p0))
+        wl = tio.load_quant(p1)
+        sb = wq.block_size
+        assert ("mma", sb) in wl._cache and (vw != "mbs_d" or "sig_t" in wl._cache)
+        fresh = tio.load_quant(p0, gemm_layout=True)
+        assert torch.equal(wl._cache[("mma", sb)], fresh._cache[("mma", sb)])
+        if vw == "mbs_d":
+            assert torch.equal(wl._cache["sig_t"], fresh._cache["sig_t"])
+        aq = M.quantize_tensor(a, M.SchemeConfig(M.Variant(va)))
+        assert torch.equal(M.matmul_quantized(aq, wq), M.matmul_quantized(aq, wl)), vw
+    # stale: another tool (e.g. the reference) rewrote the container, the
+    # MBS-D sidecar stayed
+    other = M.quantize_tensor(w * 2, M.SchemeConfig(M.Variant.MBS_D))
+    tio.save_quant(other, str(tmp_path / "other.mxq"))
+    shutil.copyfile(str(tmp_path / "other.mxq"), str(tmp_path / "mbs_d.mxq"))
+    with pytest.raises(ValueError, match="stale export"):
+        tio.load_quant(str(tmp_path / "mbs_d.mxq"))
+    # our own save without gemm_layout drops the sidecar it invalidates
+    tio.save_quant(other, str(tmp_path / "mbs_d.mxq"))
+    assert not os.path.exists(tio.layout_path(str(tmp_path / "mbs_d.mxq")))
+    assert tio.load_quant(str(tmp_path / "mbs_d.mxq")) == other
