@@ -280,7 +280,7 @@ def run_ours(args):
     # the timed launches cycle over 8 distinct activations (256 MB, twice the
     # L2), so every launch streams its input from HBM
     qbw = quantizer_bandwidth(torch, M, dev, args)
-    experts = grouped_experts(torch, M, dev, args) if (rank == 0 and args.experts) else None
+    experts = grouped_experts(torch, M, P, dev, args, world, rank, barrier) if args.experts else None
 
     out = None
     if rank == 0:
@@ -466,48 +466,65 @@ def quantizer_bandwidth(torch, M, dev, args):
     return qbw
 
 
-def grouped_experts(torch, M, dev, args):
-    """C5: GPT-OSS-120B MoE expert GEMMs (decode-sized token groups), 64
-    experts per launch, MBS-H (MBS_S tokens x MBS_D weights) vs NVFP4 x NVFP4,
-    both on the grouped tcgen05 kernel (matmul_quantized_grouped).  The 64
-    experts' weights (gate_up 5760 x 2880: 597 MB in MBS) exceed the L2, so
-    every launch streams its weights from HBM; reported as weight GB/s
-    (algorithmic weight bytes: codes + scales + MBS mantissa bytes) and
-    microseconds per expert."""
+def grouped_experts(torch, M, P, dev, args, world=1, rank=0, barrier=None):
+    """C5: GPT-OSS-120B MoE expert GEMMs (decode-sized token groups), one MoE
+    layer's 128 experts, MBS-H (MBS_S tokens x MBS_D weights) vs NVFP4 x
+    NVFP4, both on the grouped tcgen05 kernel (matmul_quantized_grouped, up
+    to 64 experts per launch).  Expert-parallel over the ranks (SURVEY §8 e:
+    128/N experts per GPU, replicas only -- the per-expert GEMMs exchange
+    nothing; 16 experts per GPU at N = 8), timed as the max over ranks of the
+    device time of one layer's launches.  Per GPU the weights (gate_up
+    5760 x 2880: 1.2 GB in MBS at N = 1) exceed the L2 at N <= 4, so every
+    launch streams its weights from HBM; reported as whole-job weight GB/s
+    (algorithmic weight bytes: codes + scales + MBS mantissa bytes), the
+    fraction of N x HBM, and microseconds per layer and per expert."""
     V = M.Variant
-    n_exp, k = 64, 2880
-    out = {}
+    n_total, k = 128, 2880
+    n_exp = n_total // world
+    first = rank * n_exp
+    out = {"experts_per_layer": n_total, "experts_per_gpu": n_exp, "n_gpus": world}
     hbm = hbm_peak()
     for proj, n in (("gate_up", 5760), ("down", 2880)):
-        gw = torch.Generator(device=dev).manual_seed(777)
-        wd = [(torch.randn(n, k, device=dev, generator=gw) * 0.02).to(torch.bfloat16) for _ in range(n_exp)]
         for arm, (av, wv) in (("mbs_h", (V.MBS_S, V.MBS_D)), ("nvfp4", (V.NVFP4, V.NVFP4))):
-            wq = [M.quantize_tensor(w, M.SchemeConfig(wv), check=False) for w in wd]
+            wq = []
+            for e in range(first, first + n_exp):  # (this rank's experts; quantized one at a time)
+                gw = torch.Generator(device=dev).manual_seed(777 + e)
+                w = (torch.randn(n, k, device=dev, generator=gw) * 0.02).to(torch.bfloat16)
+                wq.append(M.quantize_tensor(w, M.SchemeConfig(wv), check=False))
+                del w
             wbytes = n * k * (0.5 + 1 / 16 + (1 / 128 if arm == "mbs_h" else 0.0))
             for mtok in (1, 8, 32, 128):
-                gt = torch.Generator(device=dev).manual_seed(mtok)
+                gt = torch.Generator(device=dev).manual_seed(mtok * 1000 + rank)
                 toks = [M.quantize_tensor(torch.randn(mtok, k, device=dev, generator=gt).to(torch.bfloat16),
                                           M.SchemeConfig(av), check=False) for _ in range(n_exp)]
-                M.matmul_quantized_grouped(toks, wq, out_dtype=torch.bfloat16, check=False)
+
+                def layer():
+                    for g0 in range(0, n_exp, 64):
+                        M.matmul_quantized_grouped(toks[g0:g0 + 64], wq[g0:g0 + 64], out_dtype=torch.bfloat16,
+                                                   check=False)
+
+                layer()
                 torch.cuda.synchronize()
                 reps = 10
                 g = torch.cuda.CUDAGraph()  # device time of the launches (the expert table is a kernel parameter)
                 with torch.cuda.graph(g):
                     for _ in range(reps):
-                        M.matmul_quantized_grouped(toks, wq, out_dtype=torch.bfloat16, check=False)
+                        layer()
                 g.replay()
+                if barrier is not None:
+                    barrier()
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 g.replay()
                 e1.record()
                 torch.cuda.synchronize()
-                us = e0.elapsed_time(e1) / reps * 1e3
-                gbs = n_exp * wbytes / (us * 1e-6) / 1e9
-                out[f"{proj}.{arm}.m{mtok}"] = {"us_per_launch": round(us, 2), "us_per_expert": round(us / n_exp, 3),
-                                                "weight_gbs": round(gbs, 1), "hbm_frac": round(gbs / hbm, 3)}
+                us = P.max_over_ranks(e0.elapsed_time(e1) / reps * 1e3, device=dev)
+                gbs = n_total * wbytes / (us * 1e-6) / 1e9
+                out[f"{proj}.{arm}.m{mtok}"] = {"us_per_layer": round(us, 2), "us_per_expert": round(us / n_exp, 3),
+                                                "weight_gbs": round(gbs, 1), "hbm_frac": round(gbs / (hbm * world), 3)}
+                del g, toks
             del wq
-        del wd
     return out
 
 

@@ -5,6 +5,7 @@ import torch
 import paper_2603_08713_b200 as M
 import bench
 class A: pass
-r = bench.grouped_experts(torch, M, torch.device("cuda", 0), A())
+from paper_2603_08713_b200 import parallel as P
+r = bench.grouped_experts(torch, M, P, torch.device("cuda", 0), A())
 for k, v in r.items():
     print(k, v)
