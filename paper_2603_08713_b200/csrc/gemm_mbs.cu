@@ -94,7 +94,9 @@ struct MbsCfg {
   static constexpr bool SETMAXNREG = false;
 #endif
   static constexpr int EPI_REGS = EPIW == 16 ? 112 : 208, CTRL_REGS = EPIW == 16 ? 32 : 48;
-  static_assert(EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= (EPIW == 16 ? 96 * 640 : 168 * 384), "register pool");
+  // per-thread register cap at launch: the whole file fits 64K registers
+  static constexpr int MAXNREG = EPIW == 16 ? 96 : (THREADS * 168 <= 65536 ? 168 : (65536 / THREADS) & ~7);
+  static_assert(!SETMAXNREG || EPIW * 32 * EPI_REGS + 4 * 32 * CTRL_REGS <= MAXNREG * THREADS, "register pool");
   static_assert(SMEM <= 232448, "shared memory budget");
   static_assert(OFF_B % 1024 == 0 && STAGE_B % 1024 == 0 && (BN / 2) * 128 % 1024 == 0, "128B-swizzle alignment");
   static_assert(COL_SF0 + NSFB * SF_STRIDE <= 512, "TMEM budget");
@@ -700,14 +702,14 @@ __device__ __forceinline__ void mbs_body(const CUtensorMap* tmA, const CUtensorM
 }
 
 template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS, bool FUSED = false>
-__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
+__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__((MbsCfg<BN_, NB_, EPIW_>::MAXNREG))
     k_gemm_mbs(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ Params p) {
   mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, TRANS, FUSED, false>(&tmA, &tmB, p, nullptr);
 }
 
 template <int BN_, int NB_, int EPIW_, bool OUT_BF16, int CL, bool TRANS>
-__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__(EPIW_ == 16 ? 96 : 168)
+__global__ void __launch_bounds__(MbsCfg<BN_, NB_, EPIW_>::THREADS, 1) __maxnreg__((MbsCfg<BN_, NB_, EPIW_>::MAXNREG))
     k_gemm_mbs_grouped(const __grid_constant__ GroupTable gt) {
   mbs_body<BN_, NB_, EPIW_, OUT_BF16, CL, TRANS, false, true>(nullptr, nullptr, gt.p, &gt);
 }
