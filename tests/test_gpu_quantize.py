@@ -6,6 +6,8 @@ dequantised f32 values, QSNR (mse / signal f64 sums) and flush rates.
 """
 
 import hashlib
+import json
+import os
 import math
 
 import numpy as np
@@ -198,6 +200,35 @@ def test_config1_full_size_bit_exact(golden_meta, variant):
     rep, fl = M.qsnr_quantized(tb, q)
     assert rep.qsnr_db == want["qsnr_db"] and rep.mse == want["mse"] and rep.signal_power == want["signal"]
     assert fl == want["flush"]
+
+
+def _field_digest(q):
+    h = hashlib.sha256()
+    fields = {"codes": q.codes, "block_scales": q.block_scales, "e4m3_scales": q.e4m3_scales,
+              "mbs_mantissas": q.mbs_mantissas}
+    if q.tensor_scale is not None:
+        fields["tensor_scale"] = np.array([q.tensor_scale], np.float64)
+    for f in sorted(k for k, v in fields.items() if v is not None):
+        v = fields[f]
+        h.update(f.encode())
+        h.update(np.ascontiguousarray(v.cpu().numpy() if isinstance(v, torch.Tensor) else v).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("seed", range(1, 8))
+def test_config1_all_seeds(seed):
+    """C1 over seeds 1..7 (SURVEY section 8 d: "seeds 0..7"; seed 0 above):
+    every variant's quantized fields, QSNR dB and flush rate on the GPU equal
+    the reference's (tests/golden/make_qsnr_seeds.py -> qsnr_seeds.json)."""
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "qsnr_seeds.json")))["seeds"][str(seed)]
+    t = O.bf16_round(O.generate("gaussian_with_outliers", (4096, 4096), seed))
+    assert hashlib.sha256(t.tobytes()).hexdigest() == ref["sha256_bf16"]
+    tb = torch.from_numpy(t).cuda().to(torch.bfloat16)
+    for variant in ("ocp32", "mx16", "mx16_oas", "mbs_s", "mbs_d", "nvfp4"):
+        q = M.quantize_tensor(tb, M.SchemeConfig(M.Variant(variant)))
+        assert _field_digest(q) == ref[variant]["sha256"], variant
+        rep, fl = M.qsnr_quantized(tb, q)
+        assert rep.qsnr_db == ref[variant]["qsnr_db"] and fl == ref[variant]["flush"], variant
 
 
 def test_exact_gemm_matches_golden(golden, golden_meta):

@@ -78,3 +78,21 @@ def test_generator_reproduces_config1_digest(golden_meta):
     import hashlib
     t = O.bf16_round(O.generate("gaussian_with_outliers", (4096, 4096), 0))
     assert hashlib.sha256(t.tobytes()).hexdigest() == golden_meta["config1_sha256_bf16"]
+
+
+def test_generator_reproduces_config1_seed_digests():
+    """C1 over seeds 1..7: the oracle's PCG64 draw reproduces the reference's
+    bf16 tensors recorded in tests/golden/qsnr_seeds.json, and the recorded
+    mean is the reference's running-sum mean (src/metrics.py:228-246)."""
+    import hashlib
+    import json
+    import os
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "qsnr_seeds.json")))
+    for s in (1, 7):
+        t = O.bf16_round(O.generate("gaussian_with_outliers", (4096, 4096), s))
+        assert hashlib.sha256(t.tobytes()).hexdigest() == d["seeds"][str(s)]["sha256_bf16"]
+    for v, m in d["mean_qsnr_db"].items():
+        acc = 0.0
+        for s in range(8):
+            acc += d["seeds"][str(s)][v]["qsnr_db"]
+        assert acc / 8 == m
