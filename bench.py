@@ -5,7 +5,7 @@ Workload (one "step"): the four Llama-3-8B linear layers at M = 4096 tokens --
 QKV (N 6144, K 4096), O (4096, 4096), gate_up (28672, 4096), down (4096, 14336)
 -- each = quantize the bf16 activation on the fly (MBS-S) and run the tcgen05
 block-scaled GEMM against resident MBS-D weights (MBS-H, the paper's default),
-bf16 output.  Synthetic data: activations gaussian with 1% x100 outliers,
+bf16 output.  Synthetic data: activations student-t dof 4 (activation-like),
 random-init weights N(0, 0.02).  Headline `value` = step TFLOP/s (device-timed,
 inputs resident in HBM); `e2e` = the same step through the public API with
 pinned host activations in and bf16 products out.  Comparison arms on the
@@ -130,10 +130,15 @@ QWEN3_LAYERS = 36
 
 
 def synth_activation(torch, dev, rows, k, gen):
-    """N(0, 1) with 1% x100 outliers (config 1's generator), bf16."""
-    x = torch.randn(rows, k, device=dev, generator=gen)
-    hit = torch.rand(rows, k, device=dev, generator=gen) < 0.01
-    return torch.where(hit, x * 100.0, x).to(torch.bfloat16)
+    """Student-t, dof 4 -- the reference's activation-like generator
+    (src/metrics.py:103-105; SURVEY section 8 d, C2) -- drawn on the device as
+    Z / sqrt(chi2_4 / 4), chi2_4 the sum of four squared standard normals; bf16."""
+    z = torch.randn(rows, k, device=dev, generator=gen)
+    chi2 = torch.zeros_like(z)
+    for _ in range(4):
+        e = torch.randn(rows, k, device=dev, generator=gen)
+        chi2.addcmul_(e, e)
+    return (z * torch.rsqrt(chi2 * 0.25)).to(torch.bfloat16)
 
 
 # ---------------------------------------------------------------------------
@@ -344,7 +349,7 @@ def run_ours(args):
         "steps": K, "warmup": W, "ms_per_step": round(head["ms_per_step"], 4), "higher_is_better": True,
         "scaling": "strong" if cols else "weak", "vs_baseline": None,
         "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
-        "data": "synthetic (activations N(0,1) with 1% x100 outliers; random-init N(0,0.02) weights)",
+        "data": "synthetic (activations student-t dof 4, the reference's activation_like; random-init N(0,0.02) weights)",
         "config": {"workload": wl_desc, "global_batch": M_TOK * (1 if cols else world), "seq_len": None,
                    "parallelism": par,
                    "l2": "inputs larger than L2 (218 MB bf16 activations + 121 MB fp4 weights per step)"},
@@ -509,7 +514,7 @@ def grouped_experts(torch, M, P, dev, args, world=1, rank=0, barrier=None):
                 wq.append(M.quantize_tensor(w, M.SchemeConfig(wv), check=False))
                 del w
             wbytes = n * k * (0.5 + 1 / 16 + (1 / 128 if arm == "mbs_h" else 0.0))
-            for mtok in (1, 8, 32, 128):
+            for mtok in (1, 2, 4, 8, 16, 32, 64, 128):
                 gt = torch.Generator(device=dev).manual_seed(mtok * 1000 + rank)
                 toks = [M.quantize_tensor(torch.randn(mtok, k, device=dev, generator=gt).to(torch.bfloat16),
                                           M.SchemeConfig(av), check=False) for _ in range(n_exp)]
@@ -564,7 +569,7 @@ def run_e2e(torch, M, P, dev, world, args, acts, outs, wq, step_flops_global, ba
     comp = torch.cuda.current_stream()
     consumed = [[None] * n_layers for _ in range(2)]   # compute done reading dev_in[b][li]
     drained = [[None] * n_layers for _ in range(2)]    # D2H done reading dev_out[b][li]
-    statuses = []
+    status_acc = torch.zeros(1, dtype=torch.int32, device=dev)   # non-finite flags of every step
 
     def e2e_step(it):
         # H2D on one copy engine, D2H on the other, compute in between: layer
@@ -586,7 +591,11 @@ def run_e2e(torch, M, P, dev, world, args, acts, outs, wq, step_flops_global, ba
                 comp.wait_event(drained[b][li])
             # public API; the non-finite status is checked after the timed region
             aq = M.quantize_tensor(dev_in[b][li], cfg_a, check=False)
-            statuses.append(aq._cache["status"])
+            # OR the status word into one accumulator: holding the status view
+            # itself would keep the call's whole output allocation alive, and
+            # every later quantize call would then cudaMalloc (2-3 ms of host
+            # time each: the e2e leg ran host-bound at 20-60 ms per step)
+            status_acc.bitwise_or_(aq._cache["status"][:1])
             M.matmul_quantized(aq, wq[li], out=dev_out[b][li], out_dtype=bf16, check=False)
             done = torch.cuda.Event()
             done.record(comp)
@@ -599,11 +608,7 @@ def run_e2e(torch, M, P, dev, world, args, acts, outs, wq, step_flops_global, ba
                 drained[b][li] = dr
 
     W, K = args.warmup, args.steps
-    # warm-up to the steady state: after the device-only legs the first few
-    # hundred ms of copies run at a fraction of the PCIe rate (link / IOMMU
-    # warm-up; tools/e2e_probe.py: 6 warm-up steps 10.5 ms per step, 20 steps
-    # 8.6 ms, 40 steps 7.4 ms, steady state 6.9-7.1 ms)
-    for it in range(max(env_int("MXQ_E2E_WARMUP", 40), W)):
+    for it in range(max(env_int("MXQ_E2E_WARMUP", 8), W)):
         e2e_step(it)
     torch.cuda.synchronize()
     ke = max(8, K)
@@ -611,17 +616,40 @@ def run_e2e(torch, M, P, dev, world, args, acts, outs, wq, step_flops_global, ba
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    t_enq = 0.0
     for it in range(ke):
+        tq = time.perf_counter()
         e2e_step(it)
+        t_enq += time.perf_counter() - tq
     comp.wait_stream(s_d2h)   # the last step's products are on the host
     e1.record()
     torch.cuda.synchronize()
     ms_e2e = P.max_over_ranks(e0.elapsed_time(e1) / ke, device=dev)
     wall = P.max_over_ranks((time.perf_counter() - t0) * 1e3 / ke, device=dev)
-    for st in statuses:
-        M._lib.raise_on_status(st)
+    M._lib.raise_on_status(status_acc)
     host_ok = bool(torch.equal(host_out[0], dev_out[(ke - 1) % 2][0].cpu()))
+    # the link's rate in the same run, both directions at once on the two copy
+    # streams (the e2e step is bound by it; it varies between runs of one box)
+    nb = 256 << 20
+    hb = [torch.empty(nb, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    db = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+    for rep in range(2):
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        s_h2d.wait_event(f0)
+        s_d2h.wait_event(f0)
+        with torch.cuda.stream(s_h2d):
+            db[0].copy_(hb[0], non_blocking=True)
+        with torch.cuda.stream(s_d2h):
+            hb[1].copy_(db[1], non_blocking=True)
+        comp.wait_stream(s_h2d)
+        comp.wait_stream(s_d2h)
+        f1.record()
+        torch.cuda.synchronize()
+    duplex = nb / (f0.elapsed_time(f1) * 1e-3) / 1e9
+    bound_ms = max(sum(a.numel() * 2 for a in acts), sum(o.numel() * 2 for o in outs)) / (duplex * 1e9) * 1e3
     return {"value": step_flops_global / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "pcie_duplex_gbs_each_way": round(duplex, 1), "host_enqueue_ms_per_step": round(t_enq * 1e3 / ke, 3), "pcie_bound_ms_per_step": round(bound_ms, 3),
             "h2d_bytes_per_step": int(sum(a.numel() * 2 for a in acts)) * world,
             "d2h_bytes_per_step": int(sum(o.numel() * 2 for o in outs)) * world,
             "ms_per_step": ms_e2e, "wall_ms_per_step": wall, "steps": ke,
@@ -703,7 +731,7 @@ def run_layers(args, world, rank, local, dev, backend):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp4_e2m1 (UE8M0 block-16 scales, MBS sigma f32, f32 accum)",
             "data": "synthetic (random-init N(0,0.02) bf16 weights per (layer, projection); activations "
-                    "N(0,1) with 1% x100 outliers)",
+                    "student-t dof 4)",
             "config": {"workload": "qwen3-8b: 36 layers x {q,k,v,o,gate,up,down} (6.95 B params) MBS-D exact "
                                    "weight quantization + MBS-H prefill GEMMs at M=4096, per step",
                        "global_batch": M_TOK, "seq_len": None,

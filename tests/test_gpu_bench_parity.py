@@ -58,12 +58,11 @@ def check_tol(c, want, bound, tag):
 
 
 def bench_inputs(dev, k, n, seed):
-    """Bench-step operands: gaussian activations with 1% x100 outliers (bf16),
-    N(0, 0.02) random-init weights (bf16) -- bench.py's generator."""
+    """Bench-step operands: student-t dof 4 activations (bf16), N(0, 0.02)
+    random-init weights (bf16) -- bench.py's own generator."""
+    import bench
     g = torch.Generator(device=dev).manual_seed(seed)
-    x = torch.randn(M_TOK, k, device=dev, generator=g)
-    hit = torch.rand(M_TOK, k, device=dev, generator=g) < 0.01
-    a = torch.where(hit, x * 100.0, x).to(torch.bfloat16)
+    a = bench.synth_activation(torch, dev, M_TOK, k, g)
     w = (torch.randn(n, k, device=dev, generator=g) * 0.02).to(torch.bfloat16)
     return a, w
 
