@@ -113,13 +113,13 @@ __device__ __forceinline__ float load_ref(const void* ref, int dtype, int64_t of
   return reinterpret_cast<const float*>(ref)[off];
 }
 
-__global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restrict__ ref, int dtype, int64_t ref_ld,
+__global__ void __launch_bounds__(QS_THREADS, 4) k_qsnr_nodes(const void* __restrict__ ref, int dtype, int64_t ref_ld,
                                                            QDesc q, int has_q, const float* __restrict__ recon,
                                                            int64_t recon_ld, int64_t rows, int64_t cols, int depth,
                                                            double* __restrict__ ws, uint32_t* __restrict__ status) {
   __shared__ Range s_leaf[QS_MAXLEAF];
   __shared__ double s_la[QS_MAXLEAF], s_lb[QS_MAXLEAF];
-  __shared__ double s_sq[QS_WARPS][2][2][128];  // [warp][leaf slot][signal/error][element]
+  __shared__ __align__(16) double s_sq[QS_WARPS][2][2][128];  // [warp][leaf slot][signal/error][element]
   __shared__ int s_nl;
   __shared__ unsigned long long s_cnt[2];
   __shared__ Range s_stack[64];
@@ -157,44 +157,52 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
   const uint32_t ucols = (uint32_t)cols;
   const int bs_shift = has_q ? (q.block_size == 32 ? 5 : 4) : 4;
   const uint32_t umacro = has_q && q.mant ? (uint32_t)q.macro_size : 1u;
-  const bool ref_vec = dtype == DT_BF16 && (ref_ld % 4) == 0 && ((uintptr_t)ref % 8) == 0;
-  // Two leaves per warp iteration: their element loads overlap, and the two
-  // leaves' numpy-order accumulator chains run side by side (lanes 0-15 on
-  // leaf t = 0, lanes 16-31 on t = 1) -- the chains, not the loads, bound
-  // this kernel.
+  // Two leaves per warp iteration, eight consecutive elements per lane (lanes
+  // 0-15 on leaf li, 16-31 on leaf li + QS_WARPS): a lane's eight elements lie
+  // in one row, one 16-block and one macro (leaves start at multiples of 8,
+  // rows are multiples of 16 long), so its index math, scale / mantissa loads
+  // and dequantisation quotients are done once per eight elements and its
+  // reference / code loads are one 16-byte and one 4-byte load.  The two
+  // leaves' numpy-order accumulator chains then run side by side.
+  const int64_t node_r = node.s / cols;
+  const uint32_t node_c = (uint32_t)(node.s - node_r * cols);
+  const bool row8 = (ucols % 8u) == 0u;  // (always, with a quantized operand: cols % 16 == 0)
+  const bool ref_vec8 = dtype == DT_BF16 && (ref_ld % 8) == 0 && ((uintptr_t)ref % 16) == 0;
+  const bool codes_vec = has_q && (q.codes_ld % 4) == 0 && ((uintptr_t)q.codes % 4) == 0;
+  const bool mac_pow2 = (umacro & (umacro - 1)) == 0;
+  const int mac_shift = __ffs((int)umacro) - 1;
   for (int li = warp; li < nl; li += 2 * QS_WARPS) {
+    {
+      const int t = lane >> 4, lj = li + t * QS_WARPS;
+      const int p0 = 8 * (lane & 15);
+      double a8[8], b8[8];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int lj = li + t * QS_WARPS;
-      if (lj >= nl) break;
-      const Range lf = implicit ? Range{node.s + 128 * (int64_t)lj, 128} : s_leaf[lj];
-      const int64_t row0 = lf.s / cols;
-      const uint32_t c0 = (uint32_t)(lf.s - row0 * cols);
-      // A lane's 4 elements (p0..p0+3) lie in one row and one 16-block: leaves
-      // start at multiples of 8 and rows are multiples of 16 long.  Row, block,
-      // scale, mantissa and the two dequantisation quotients are computed once
-      // per lane per leaf (the first version spent ~220 instructions per element
-      // on per-element index math and divisions).
-      const int p0 = 4 * lane;
-      double a4[4] = {0.0, 0.0, 0.0, 0.0}, b4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int j = 0; j < 8; ++j) a8[j] = b8[j] = 0.0;
+      const Range lf = lj < nl ? (implicit ? Range{node.s + 128 * (int64_t)lj, 128} : s_leaf[lj]) : Range{0, 0};
       if (p0 < lf.n) {
-        const uint32_t cc = c0 + (uint32_t)p0;
-        const uint32_t dr = ucols >= 128u ? (cc >= ucols ? 1u : 0u) : cc / ucols;
-        const int64_t r = row0 + dr;
+        const uint32_t cc = node_c + (uint32_t)(lf.s - node.s) + (uint32_t)p0;
+        const uint32_t dr = cc < ucols ? 0u : cc / ucols;
+        const int64_t r = node_r + dr;
         const uint32_t c = cc - dr * ucols;
-        float xv[4];
-        uint32_t codes4 = 0x1111u;  // (dense recon: no flush statistics)
+        float xv[8];
+        uint32_t codes8 = 0x11111111u;  // (dense recon: no flush statistics)
         if (has_q) {
           const uint8_t* cp = q.codes + r * q.codes_ld + (c >> 1);
-          codes4 = (uint32_t)*reinterpret_cast<const uint16_t*>(cp);  // (c is a multiple of 4: 2-byte aligned)
+          if (codes_vec) {
+            codes8 = *reinterpret_cast<const uint32_t*>(cp);
+          } else {
+            codes8 = 0u;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) codes8 |= (uint32_t)cp[j] << (8 * j);
+          }
           const uint32_t sc = q.scales[r * q.scales_ld + (c >> bs_shift)];
           if (q.variant == NVFP4) {
             bad |= ((sc & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
-  #pragma unroll
-            for (int j = 0; j < 4; ++j) xv[j] = deq_nvfp4((codes4 >> (4 * j)) & 15u, sc, st);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xv[j] = deq_nvfp4((codes8 >> (4 * j)) & 15u, sc, st);
           } else {
             bad |= (sc == 255u) ? ST_BAD_E8M0 : 0u;
-            const uint32_t m8 = q.mant ? q.mant[r * q.mant_ld + c / umacro] : 0u;
+            const uint32_t m8 = q.mant ? q.mant[r * q.mant_ld + (mac_pow2 ? (c >> mac_shift) : c / umacro)] : 0u;
             if (sc >= 4u && sc <= 250u) {
               // exact: every magnitude is RN(1/f) or RN(1.5/f) times a power of
               // two (see k_dequantize)
@@ -204,54 +212,71 @@ __global__ void __launch_bounds__(QS_THREADS) k_qsnr_nodes(const void* __restric
                 u = uv.x;
                 v = uv.y;
               }
-  #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const uint32_t code = (codes4 >> (4 * j)) & 15u, idx = code & 7u;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t code = (codes8 >> (4 * j)) & 15u, idx = code & 7u;
                 const float base = ((idx & 1u) && idx > 1u) ? v : u;
                 const float mag =
                     idx ? base * __uint_as_float((uint32_t)((int)(idx >> 1) - 1 + (int)sc) << 23) : 0.0f;
                 xv[j] = (code & 8u) ? -mag : mag;
               }
             } else {
-  #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const uint32_t code = (codes4 >> (4 * j)) & 15u;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const uint32_t code = (codes8 >> (4 * j)) & 15u;
                 xv[j] = q.mant ? deq_mbs(code, sc, m8) : deq_pow2(code, sc);
               }
             }
           }
-        } else {
-  #pragma unroll
-          for (int j = 0; j < 4; ++j) xv[j] = recon[r * recon_ld + c + j];
+        } else if (row8) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xv[j] = recon[r * recon_ld + c + j];
         }
-        float rv4[4];
-        if (ref_vec) {  // four bf16 (8 bytes) in one load
-          const uint2 w = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(ref) + r * ref_ld + c);
-          rv4[0] = __uint_as_float(w.x << 16);
-          rv4[1] = __uint_as_float(w.x & 0xFFFF0000u);
-          rv4[2] = __uint_as_float(w.y << 16);
-          rv4[3] = __uint_as_float(w.y & 0xFFFF0000u);
+        float rv8[8];
+        if (!row8) {
+          // dense reconstruction with rows not a multiple of 8 long: the
+          // lane's elements may cross rows, index each one
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t e = cc + (uint32_t)j, dj = e / ucols;
+            const int64_t rj = node_r + dj;
+            const uint32_t cj = e - dj * ucols;
+            xv[j] = recon[rj * recon_ld + cj];
+            rv8[j] = load_ref(ref, dtype, rj * ref_ld + cj);
+          }
+        } else if (ref_vec8) {  // eight bf16 (16 bytes) in one load
+          const uint4 w = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(ref) + r * ref_ld + c);
+          const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            rv8[2 * j] = __uint_as_float(wv[j] << 16);
+            rv8[2 * j + 1] = __uint_as_float(wv[j] & 0xFFFF0000u);
+          }
         } else {
-  #pragma unroll
-          for (int j = 0; j < 4; ++j) rv4[j] = load_ref(ref, dtype, r * ref_ld + c + j);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rv8[j] = load_ref(ref, dtype, r * ref_ld + c + j);
         }
-  #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float rv = rv4[j];
+        uint32_t nz8 = 0, fl8 = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float rv = rv8[j];
           const double r64 = (double)rv;
           const double d = __dsub_rn(r64, (double)xv[j]);
-          a4[j] = __dmul_rn(r64, r64);
-          b4[j] = __dmul_rn(d, d);
-          if (rv != 0.0f) {
-            ++nz;
-            if (((codes4 >> (4 * j)) & 7u) == 0) ++fl;
-          }
+          a8[j] = __dmul_rn(r64, r64);
+          b8[j] = __dmul_rn(d, d);
+          const uint32_t isnz = rv != 0.0f ? 1u : 0u;
+          nz8 += isnz;
+          fl8 += (((codes8 >> (4 * j)) & 7u) == 0u) ? isnz : 0u;
         }
+        nz += nz8;
+        fl += fl8;
       }
-  #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        s_sq[warp][t][0][p0 + j] = a4[j];
-        s_sq[warp][t][1][p0 + j] = b4[j];
+      double* sa = &s_sq[warp][t][0][p0];
+      double* sb = &s_sq[warp][t][1][p0];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        *reinterpret_cast<double2*>(sa + j) = make_double2(a8[j], a8[j + 1]);
+        *reinterpret_cast<double2*>(sb + j) = make_double2(b8[j], b8[j + 1]);
       }
     }
     __syncwarp();

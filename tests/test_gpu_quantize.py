@@ -108,6 +108,21 @@ def test_qsnr_kats():
         M.qsnr_tensor(ref, ref[:, :16])
 
 
+@pytest.mark.parametrize("shape", [(3, 40), (7, 24), (5, 1000), (130, 12), (2, 36868), (4096, 6)])
+def test_qsnr_dense_ragged_rows(shape):
+    """qsnr_tensor on dense reconstructions whose rows are not a multiple of
+    8 (or 16) long: the evaluator's per-element indexing branch, bit-exact to
+    numpy's pairwise sums (src/metrics.py:127-153)."""
+    if (shape[0] * shape[1]) % 8:
+        pytest.skip("the GPU evaluator takes element counts that are multiples of 8")
+    rng = np.random.Generator(np.random.PCG64(shape[0] * 7 + shape[1]))
+    ref = rng.standard_t(4, shape).astype(np.float32)
+    rec = (ref + rng.standard_normal(shape).astype(np.float32) * 0.01).astype(np.float32)
+    rep = M.qsnr_tensor(ref, rec)
+    want = O.qsnr(ref, rec)
+    assert (rep.qsnr_db, rep.mse, rep.signal_power) == want
+
+
 def test_e2m1_hardware_conversion_kat():
     """cvt.rn.satfinite.e2m1x2.f32 + the -0 fix against the reference encoder
     on every midpoint, its f32 neighbours, tiny values, saturation and both
