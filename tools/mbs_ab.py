@@ -1,6 +1,7 @@
 """A/B device timing of the MBS-H GEMM (MBS_S x MBS_D) on the Llama-3-8B
 layer shapes and 8192^3, against the plain MX16_OAS / OCP32 kernels
-(development aid; MXQ_GEMM_MBS_V1=1 selects the first-generation MBS kernel)."""
+(development aid; MXQ_LIB_PATH selects a tools/build_variant.sh build, see
+tools/probe_ab.sh)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -1,6 +1,7 @@
-"""clock64 trace of the 128x128 MBS GEMM (k_gemm_mbs2) hand-offs in CTA 0
-(development aid; run with MXQ_LIB_PATH=tools/_bin/libmxq200_trace.so, built by
-tools/build_variant.sh trace -DMXQ_GEMM_TRACE=1).  Slots per chunk q:
+"""clock64 trace of the MBS GEMM (k_gemm_mbs, 128x192 tiles, two TMEM partial
+buffers) hand-offs in CTA 0 (development aid; run with
+MXQ_LIB_PATH=tools/_bin/libmxq200_trace.so, built by
+tools/build_variant.sh trace -DMXQ_GEMM_TRACE=1; profiles/r02_trace_mbs_8192.txt).  Slots per chunk q:
 0/1 MMA before/after tempty wait, 10 MMA after stage-full wait, 2 MMA after
 tfull commit; 3/4 epilogue warp 0 before/after tfull wait (then LDTM issue),
 5 after release (arrive tempty), 6 after sigma wait, 7 fold end; 8/9 last
@@ -40,7 +41,7 @@ print("median chunk period (epi_go):", med(np.diff(t[sl, 4])), " mma_go:", med(n
 print("MMA wait tempty:", med(t[sl, 1] - t[sl, 0]), " MMA go->commit:", med(t[sl, 2] - t[sl, 1]))
 print("epi wait tfull:", med(t[sl, 4] - t[sl, 3]), " epi go(c)->release(c) [LDTM + fold(c-1)]:", med(t[sl, 5] - t[sl, 4]))
 print("epi release->sig ok:", med(t[sl, 6] - t[sl, 5]), " fold:", med(t[sl, 7] - t[sl, 6]))
-print("release(c) -> MMA go(c+3):", med(t[103:403, 1] - t[100:400, 5]), " w7:", med(t[103:403, 1] - t[100:400, 9]))
+print("release(c) -> MMA go(c+2):", med(t[102:402, 1] - t[100:400, 5]), " w15:", med(t[102:402, 1] - t[100:400, 9]))
 print("MMA commit(c) -> epi go(c):", med(t[sl, 4] - t[sl, 2]), " w7:", med(t[sl, 8] - t[sl, 2]))
 print("w7 rel - w0 rel:", med(t[sl, 9] - t[sl, 5]))
 st = t[100:400, 12]; st = st[st > 0]
