@@ -79,6 +79,11 @@ class Clocks:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes up to a second to print its first line: start the
+            # timed work only once sampling runs, so the whole region is covered
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
         return self
@@ -290,8 +295,11 @@ def run_ours(args):
     # ---- quantizer bandwidth (4096x4096 bf16 activations, HBM-cold) -------
     # the timed launches cycle over 8 distinct activations (256 MB, twice the
     # L2), so every launch streams its input from HBM
-    qbw = quantizer_bandwidth(torch, M, dev, args)
-    experts = grouped_experts(torch, M, P, dev, args, world, rank, barrier) if args.experts else None
+    # (the clock sampler also covers the quantizer and C5 timed regions)
+    with Clocks(local) as clocks2:
+        qbw = quantizer_bandwidth(torch, M, dev, args)
+        experts = grouped_experts(torch, M, P, dev, args, world, rank, barrier) if args.experts else None
+    clocks.lines += clocks2.lines
 
     out = None
     if rank == 0:
