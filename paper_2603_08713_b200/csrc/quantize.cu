@@ -725,10 +725,20 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
   // the LUT in shared memory: a dynamically indexed kernel parameter would be
   // copied to local memory per thread
   __shared__ float s_lut[LUT ? 2 * 16 * 64 : 1];
+  // (RN(1/f), RN(1.5/f)) per mantissa byte: every dequantised magnitude
+  // RN(g/f) of the E2M1 grid g = {0.5,1,1.5,2,3,4,6} is one of the two times a
+  // power of two (exact: g/f lies in [0.25, 12], f32-normal), so a trial's
+  // eight levels need no division
+  __shared__ float2 s_uv[LUT ? 1 : 256];
   if constexpr (LUT) {
     for (int i = threadIdx.x; i < 2 * 16 * 64; i += MBSD_THREADS) s_lut[i] = (&tab.lut[0][0][0])[i];
-    __syncthreads();
+  } else {
+    for (int i = threadIdx.x; i < 256; i += MBSD_THREADS) {
+      const float f = mbs_factor((uint32_t)i);
+      s_uv[i] = make_float2(__fdiv_rn(1.0f, f), __fdiv_rn(1.5f, f));
+    }
   }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int sub = lane & (g.G - 1);
   double* gbase = s_sq + (threadIdx.x - sub) * MBSD_STRIDE;  // this group's slots
@@ -804,8 +814,16 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
         float tq[8];
         if (fast) {
           const float d = exp2i_f32((int)biased - 127);
-#pragma unroll
-          for (int k = 0; k < 8; ++k) tq[k] = __fmul_rn(__fdiv_rn(e2m1_grid(k), f), d);
+          const float2 uv = s_uv[m8];
+          const float u = uv.x * d, w = uv.y * d;  // (exact: d is a power of two in the normal range)
+          tq[0] = 0.0f;
+          tq[1] = 0.5f * u;
+          tq[2] = u;
+          tq[3] = w;
+          tq[4] = 2.0f * u;
+          tq[5] = 2.0f * w;
+          tq[6] = 4.0f * u;
+          tq[7] = 4.0f * w;
         }
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
@@ -833,9 +851,11 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
         // then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles -- the same
         // operations in the same order as pw_leaf, 16 dependent adds per lane
         // instead of 128 by one lane
-        double r = sq_at(gbase, sub);
+        // element sub + 8k sits in lane slot k/2, position sub + 8 (k % 2)
+        const double* cb = gbase + sub;
+        double r = cb[0];
 #pragma unroll
-        for (int k = 1; k < 16; ++k) r = __dadd_rn(r, sq_at(gbase, sub + 8 * k));
+        for (int k = 1; k < 16; ++k) r = __dadd_rn(r, cb[(k >> 1) * MBSD_STRIDE + 8 * (k & 1)]);
         r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));  // r0+r1, r2+r3, ...
         r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 2));  // (r0+r1)+(r2+r3), ...
         r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 4));  // the macro's sum at sub 0
