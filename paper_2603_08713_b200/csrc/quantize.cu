@@ -730,6 +730,13 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
   // power of two (exact: g/f lies in [0.25, 12], f32-normal), so a trial's
   // eight levels need no division
   __shared__ float2 s_uv[LUT ? 1 : 256];
+#ifndef MXQ_MBSD_SMEM_TQ
+#define MXQ_MBSD_SMEM_TQ 1
+#endif
+  // per-lane signed dequantisation levels of the current trial as f64 (code
+  // 0..15 -> value): one shared load per element instead of a select chain
+  // over a dynamically indexed register array and a conversion
+  __shared__ double s_tq[(LUT || !MXQ_MBSD_SMEM_TQ) ? 1 : MBSD_THREADS * 17];
   if constexpr (LUT) {
     for (int i = threadIdx.x; i < 2 * 16 * 64; i += MBSD_THREADS) s_lut[i] = (&tab.lut[0][0][0])[i];
   } else {
@@ -825,6 +832,23 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
           tq[6] = 4.0f * u;
           tq[7] = 4.0f * w;
         }
+        if (MXQ_MBSD_SMEM_TQ && fast) {
+          double* tqd = s_tq + threadIdx.x * 17;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            tqd[k] = (double)tq[k];
+            tqd[8 + k] = -(double)tq[k];
+          }
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            const uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double diff = __dsub_rn(tqd[(c2 >> (4 * h)) & 15u], (double)v[i + h]);
+              mine[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
+            }
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < 16; i += 2) {
           uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
@@ -841,6 +865,7 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
             const double diff = __dsub_rn((double)dq, (double)v[i + h]);
             mine[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
           }
+        }
         }
       }
       __syncwarp();
