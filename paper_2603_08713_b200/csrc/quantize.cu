@@ -713,6 +713,29 @@ struct MbsdTables {
   float lut[2][16][64];
 };
 
+// LUT bin of v = |x| * SF (src/quantize.py:507-542) as a byte: bit 7 the
+// regime (v >= 1), bits 0-5 the bin -- floor(v * 64) below 1,
+// floor((v - 1) * 64 / 7) above.  v is exact in f32 wherever a bin can be
+// nonzero (an f32 x times a power of two; an f32-subnormal v is below 2^-126
+// and lands in bin 0 either way), v - 1 and the products by 64 and 7 are
+// exact, and floor(RN64(t / 7)) == floor(t / 7) (t has a 24-bit significand,
+// so t / 7 is never within an f64 half-ulp of an integer from below) -- the
+// reference's f64 division per element becomes an f32 estimate with an exact
+// integer correction.
+__device__ __forceinline__ uint32_t lut_bin_byte(float x, float sf) {
+  const float vf = fabsf(x) * sf;
+  if (vf < 1.0f) {
+    const int b = (int)(vf * 64.0f);
+    return (uint32_t)(b > 63 ? 63 : b);
+  }
+  const float tt = (vf - 1.0f) * 64.0f;
+  int b = (int)(tt * 0.142857142857142857f);
+  if (7.0f * (float)(b + 1) <= tt) ++b;
+  else if (7.0f * (float)b > tt) --b;
+  b = b < 0 ? 0 : (b > 63 ? 63 : b);
+  return 0x80u | (uint32_t)b;
+}
+
 // LUT=false: exact SSE search (src/quantize.py:438-461).
 // LUT=true : table-estimated cost sum(x^2 * T[v]) (src/quantize.py:507-542),
 //            v = |x| * SF(OAS scale of the candidate-scaled block).
@@ -737,6 +760,7 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
   // 0..15 -> value): one shared load per element instead of a select chain
   // over a dynamically indexed register array and a conversion
   __shared__ double s_tq[(LUT || !MXQ_MBSD_SMEM_TQ) ? 1 : MBSD_THREADS * 17];
+  __shared__ double s_x2[LUT ? MBSD_THREADS * 17 : 1];
   if constexpr (LUT) {
     for (int i = threadIdx.x; i < 2 * 16 * 64; i += MBSD_THREADS) s_lut[i] = (&tab.lut[0][0][0])[i];
   } else {
@@ -775,48 +799,58 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
     const int n_trials = n_cand + (augment ? 1 : 0);
     double best_sse = 0.0;
     uint32_t best_m8 = 0;
+    // LUT mode: x^2 (f64, the reference's first product) and the bin bytes of
+    // |x| * SF for the two scale exponents a trial can take, once per macro
+    uint32_t lut_b0 = 0, lut_bins[2][4] = {{0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u}};
+    double* x2s = s_x2 + threadIdx.x * 17;
+    if constexpr (LUT) {
+      lut_b0 = e8m0_biased_16(a16, true);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float sfe = exp2i_f32(127 - (int)(lut_b0 + e));
+#pragma unroll
+        for (int i = 0; i < 16; ++i) lut_bins[e][i >> 2] |= lut_bin_byte(v[i], sfe) << (8 * (i & 3));
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const double x64 = (double)v[i];
+        x2s[i] = __dmul_rn(x64, x64);
+      }
+    }
     for (int t = 0; t < n_trials; ++t) {
       const uint32_t m8 = t < n_cand ? (uint32_t)tab.cands[t] : m8_static;
       const float f = mbs_factor(m8);
-      // quantise: y = x*f, OAS scale, codes
-      float y[16];
-      float a = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        y[i] = __fmul_rn(v[i], f);
-        a = fmaxf(a, fabsf(y[i]));
-      }
+      // quantise: y = x*f, OAS scale, codes.  max|RN(x f)| = RN(max|x| f)
+      // (RN is monotone), so the block maximum needs no pass over y
+      const float a = __fmul_rn(a16, f);
       const uint32_t biased = e8m0_biased_16(a, true);
       const float sf = exp2i_f32(127 - (int)biased);
       if constexpr (LUT) {
-        // bin of v = |x| * SF (src/quantize.py:507-542): floor(v * 64) below 1,
-        // floor((v - 1) * 64 / 7) above.  v is exact in f32 wherever a bin can
-        // be nonzero (an f32 x times a power of two; an f32-subnormal v is
-        // below 2^-126 and lands in bin 0 either way), v - 1 and the products
-        // by 64 and 7 are exact, and floor(RN64(t / 7)) == floor(t / 7) (t has
-        // a 24-bit significand, so t / 7 is never within an f64 half-ulp of
-        // an integer from below) -- the reference's f64 division per element
-        // becomes an f32 estimate with an exact integer correction.
+        // f < 2, so the trial's scale exponent is b0 or b0 + 1: the bins of
+        // both were taken once per macro (lut_bins); other exponents (none
+        // expected) take the per-element computation below
+        const uint32_t e = biased - lut_b0;
+        if (e <= 1u) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float vf = fabsf(v[i]) * sf;
-          float tv;
-          if (vf < 1.0f) {
-            int b = (int)(vf * 64.0f);
-            b = b > 63 ? 63 : b;
-            tv = s_lut[(0 * 16 + t) * 64 + b];
-          } else {
-            const float tt = (vf - 1.0f) * 64.0f;
-            int b = (int)(tt * 0.142857142857142857f);
-            if (7.0f * (float)(b + 1) <= tt) ++b;
-            else if (7.0f * (float)b > tt) --b;
-            b = b < 0 ? 0 : (b > 63 ? 63 : b);
-            tv = s_lut[(1 * 16 + t) * 64 + b];
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t word = e ? lut_bins[1][i >> 2] : lut_bins[0][i >> 2];
+            const uint32_t byte = (word >> (8 * (i & 3))) & 0xFFu;
+            const float tv = s_lut[((byte >> 7) * 16 + t) * 64 + (byte & 63u)];
+            mine[i] = active ? __dmul_rn(x2s[i], (double)tv) : 0.0;
           }
-          const double x64 = (double)v[i];
-          mine[i] = active ? __dmul_rn(__dmul_rn(x64, x64), (double)tv) : 0.0;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const uint32_t byte = lut_bin_byte(v[i], sf);
+            const float tv = s_lut[((byte >> 7) * 16 + t) * 64 + (byte & 63u)];
+            mine[i] = active ? __dmul_rn(x2s[i], (double)tv) : 0.0;
+          }
         }
-      } else {
+      }
+      if constexpr (!LUT) {
+        float y[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) y[i] = __fmul_rn(v[i], f);
         const bool fast = biased >= 4 && biased <= 250;
         float tq[8];
         if (fast) {

@@ -180,6 +180,24 @@ def test_row_partition_and_launch_invariance():
         assert full == M.quantize_tensor(t, cfg)
 
 
+def test_mbs_d_lut_matches_oracle_on_random_macros():
+    """f2 (the LUT-mode MBS-D, src/quantize.py:507-542) on 5,000 random
+    macros spanning many scale exponents (incl. tiny and huge blocks, so bins
+    of both regimes and both per-macro scale exponents are hit): the chosen
+    mantissa bytes equal the oracle's LUT selector."""
+    rng = np.random.Generator(np.random.PCG64(57))
+    macros = np.concatenate([
+        rng.standard_normal((2000, 128)), rng.standard_t(4, (2000, 128)),
+        np.where(rng.random((1000, 128)) < 0.01, rng.standard_normal((1000, 128)) * 100,
+                 rng.standard_normal((1000, 128)))])
+    macros *= np.exp2(rng.integers(-60, 60, (5000, 1)))
+    macros = macros.astype(np.float32)
+    cands = tuple(range(0, 256, 16))
+    q = M.quantize_tensor(macros, M.SchemeConfig(M.Variant.MBS_D, mbs_mode="lut"))
+    want = O.choose_lut(macros, O.build_lut(cands), cands)
+    assert np.array_equal(_np(q.mbs_mantissas).ravel(), want)
+
+
 def test_mbs_d_matches_oracle_on_random_macros():
     """Criterion 5 (tests/test_acceptance.py:148-168) on the GPU path."""
     rng = np.random.Generator(np.random.PCG64(55))
