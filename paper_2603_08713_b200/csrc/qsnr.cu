@@ -286,8 +286,14 @@ __global__ void __launch_bounds__(QS_THREADS, 4) k_qsnr_nodes(const void* __rest
     if (lj < nl) {
       const double* v = s_sq[warp][t][(lane >> 3) & 1];
       const int j = lane & 7, ln = implicit ? 128 : (int)s_leaf[lj].n;
-      acc = v[j];
-      for (int i = 8; i < ln; i += 8) acc = __dadd_rn(acc, v[i + j]);
+      const double* vj = v + j;
+      acc = vj[0];
+      if (ln == 128) {  // full leaf: fifteen adds at constant offsets
+#pragma unroll 5
+        for (int i = 8; i < 128; i += 8) acc = __dadd_rn(acc, vj[i]);
+      } else {
+        for (int i = 8; i < ln; i += 8) acc = __dadd_rn(acc, vj[i]);
+      }
     }
     const int base = lane & 24;
     double r0 = __shfl_sync(0xffffffffu, acc, base | 0), r1 = __shfl_sync(0xffffffffu, acc, base | 1);
