@@ -951,12 +951,28 @@ __global__ void __launch_bounds__(256) k_dequantize(QDesc q, float* __restrict__
   const int bs = q.block_size;
   const uint32_t nbr = fd_nbr.d;
   const double st = (q.variant == NVFP4 && q.tensor_scale) ? *q.tensor_scale : 1.0;
+  // (RN(1/f), RN(1.5/f)) per mantissa byte, shared by the CTA (two f32
+  // divisions per block otherwise)
+  __shared__ float2 s_uv[256];
+  if (q.mant) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      const float f = mbs_factor((uint32_t)i);
+      s_uv[i] = make_float2(__fdiv_rn(1.0f, f), __fdiv_rn(1.5f, f));
+    }
+    __syncthreads();
+  }
+  const uint32_t umac = (uint32_t)q.macro_size;
+  const bool mac_pow2 = (umac & (umac - 1)) == 0;
+  const int mac_shift = __ffs((int)umac) - 1;
   uint32_t bad = 0;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
     const uint32_t r = fdiv(b, fd_nbr), kb = b - r * nbr;
     const uint32_t s = q.scales[(int64_t)r * q.scales_ld + kb];
     uint32_t m8 = 0;
-    if (q.mant) m8 = q.mant[(int64_t)r * q.mant_ld + (kb * bs) / q.macro_size];
+    if (q.mant) {
+      const uint32_t col = kb * (uint32_t)bs;
+      m8 = q.mant[(int64_t)r * q.mant_ld + (mac_pow2 ? (col >> mac_shift) : col / umac)];
+    }
     if (q.variant == NVFP4) bad |= ((s & 0x7fu) == 0x7fu) ? ST_BAD_E4M3 : 0u;
     else bad |= (s == 255u) ? ST_BAD_E8M0 : 0u;
     // Fast path (E8M0 variants, 4 <= biased <= 250, every value f32-normal):
@@ -967,9 +983,9 @@ __global__ void __launch_bounds__(256) k_dequantize(QDesc q, float* __restrict__
     const bool fast = q.variant != NVFP4 && s >= 4u && s <= 250u;
     float u = 1.0f, v = 1.5f;
     if (fast && q.mant) {
-      const float f = mbs_factor(m8);
-      u = __fdiv_rn(1.0f, f);
-      v = __fdiv_rn(1.5f, f);
+      const float2 uv = s_uv[m8];
+      u = uv.x;
+      v = uv.y;
     }
     const uint8_t* cp = q.codes + (int64_t)r * q.codes_ld + kb * (bs / 2);
     float* op = out + (int64_t)r * out_ld + (int64_t)kb * bs;
