@@ -662,6 +662,10 @@ __global__ void __launch_bounds__(SQ_THREADS) k_stream_nvfp4(const void* __restr
 // ---------------------------------------------------------------------------
 constexpr int MBSD_THREADS = 128;
 constexpr int MBSD_STRIDE = 17;  // doubles per lane slot (16 + 1 pad)
+constexpr int MBSD_BUF = MBSD_THREADS * MBSD_STRIDE;  // one trial's staged errors
+#ifndef MXQ_MBSD_PAIR
+#define MXQ_MBSD_PAIR 1
+#endif
 
 // Element p of a macro lives in lane p/16, slot p%16.
 __device__ __forceinline__ double sq_at(const double* base, int64_t p) {
@@ -740,11 +744,11 @@ __device__ __forceinline__ uint32_t lut_bin_byte(float x, float sf) {
 // LUT=true : table-estimated cost sum(x^2 * T[v]) (src/quantize.py:507-542),
 //            v = |x| * SF(OAS scale of the candidate-scaled block).
 template <bool LUT>
-__global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __restrict__ x, int dtype, int64_t x_ld,
+__global__ void __launch_bounds__(MBSD_THREADS, LUT ? 5 : 4) k_quantize_mbs_d(const void* __restrict__ x, int dtype, int64_t x_ld,
                                                                  QDesc q, MacroGeom g, int n_cand, int augment,
                                                                  uint32_t* __restrict__ status,
                                                                  const __grid_constant__ MbsdTables tab) {
-  __shared__ double s_sq[MBSD_THREADS * MBSD_STRIDE];
+  __shared__ double s_sq[((!LUT && MXQ_MBSD_PAIR) ? 2 : 1) * MBSD_BUF];
   // the LUT in shared memory: a dynamically indexed kernel parameter would be
   // copied to local memory per thread
   __shared__ float s_lut[LUT ? 2 * 16 * 64 : 1];
@@ -759,7 +763,8 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
   // per-lane signed dequantisation levels of the current trial as f64 (code
   // 0..15 -> value): one shared load per element instead of a select chain
   // over a dynamically indexed register array and a conversion
-  __shared__ double s_tq[(LUT || !MXQ_MBSD_SMEM_TQ) ? 1 : MBSD_THREADS * 17];
+  using tq_t = typename std::conditional<MXQ_MBSD_PAIR != 0, float, double>::type;  // (48 KB static limit)
+  __shared__ tq_t s_tq[(LUT || !MXQ_MBSD_SMEM_TQ) ? 1 : MBSD_THREADS * 17];
   __shared__ double s_x2[LUT ? MBSD_THREADS * 17 : 1];
   if constexpr (LUT) {
     for (int i = threadIdx.x; i < 2 * 16 * 64; i += MBSD_THREADS) s_lut[i] = (&tab.lut[0][0][0])[i];
@@ -817,116 +822,144 @@ __global__ void __launch_bounds__(MBSD_THREADS) k_quantize_mbs_d(const void* __r
         x2s[i] = __dmul_rn(x64, x64);
       }
     }
-    for (int t = 0; t < n_trials; ++t) {
-      const uint32_t m8 = t < n_cand ? (uint32_t)tab.cands[t] : m8_static;
-      const float f = mbs_factor(m8);
-      // quantise: y = x*f, OAS scale, codes.  max|RN(x f)| = RN(max|x| f)
-      // (RN is monotone), so the block maximum needs no pass over y
-      const float a = __fmul_rn(a16, f);
-      const uint32_t biased = e8m0_biased_16(a, true);
-      const float sf = exp2i_f32(127 - (int)biased);
-      if constexpr (LUT) {
-        // f < 2, so the trial's scale exponent is b0 or b0 + 1: the bins of
-        // both were taken once per macro (lut_bins); other exponents (none
-        // expected) take the per-element computation below
-        const uint32_t e = biased - lut_b0;
-        if (e <= 1u) {
+    // One trial's per-element pass: the quantise-dequantise (or LUT) squared
+    // errors of this lane's 16 elements into mb (this lane's slots of a buffer).
+    auto elem_pass = [&](int t, double* mb) -> uint32_t {
+        const uint32_t m8 = t < n_cand ? (uint32_t)tab.cands[t] : m8_static;
+        const float f = mbs_factor(m8);
+        // quantise: y = x*f, OAS scale, codes.  max|RN(x f)| = RN(max|x| f)
+        // (RN is monotone), so the block maximum needs no pass over y
+        const float a = __fmul_rn(a16, f);
+        const uint32_t biased = e8m0_biased_16(a, true);
+        const float sf = exp2i_f32(127 - (int)biased);
+        if constexpr (LUT) {
+          // f < 2, so the trial's scale exponent is b0 or b0 + 1: the bins of
+          // both were taken once per macro (lut_bins); other exponents (none
+          // expected) take the per-element computation below
+          const uint32_t e = biased - lut_b0;
+          if (e <= 1u) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t word = e ? lut_bins[1][i >> 2] : lut_bins[0][i >> 2];
-            const uint32_t byte = (word >> (8 * (i & 3))) & 0xFFu;
-            const float tv = s_lut[((byte >> 7) * 16 + t) * 64 + (byte & 63u)];
-            mine[i] = active ? __dmul_rn(x2s[i], (double)tv) : 0.0;
-          }
-        } else {
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t word = e ? lut_bins[1][i >> 2] : lut_bins[0][i >> 2];
+              const uint32_t byte = (word >> (8 * (i & 3))) & 0xFFu;
+              const float tv = s_lut[((byte >> 7) * 16 + t) * 64 + (byte & 63u)];
+              mb[i] = active ? __dmul_rn(x2s[i], (double)tv) : 0.0;
+            }
+          } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t byte = lut_bin_byte(v[i], sf);
-            const float tv = s_lut[((byte >> 7) * 16 + t) * 64 + (byte & 63u)];
-            mine[i] = active ? __dmul_rn(x2s[i], (double)tv) : 0.0;
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t byte = lut_bin_byte(v[i], sf);
+              const float tv = s_lut[((byte >> 7) * 16 + t) * 64 + (byte & 63u)];
+              mb[i] = active ? __dmul_rn(x2s[i], (double)tv) : 0.0;
+            }
           }
         }
-      }
-      if constexpr (!LUT) {
-        float y[16];
+        if constexpr (!LUT) {
+          float y[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) y[i] = __fmul_rn(v[i], f);
-        const bool fast = biased >= 4 && biased <= 250;
-        float tq[8];
-        if (fast) {
-          const float d = exp2i_f32((int)biased - 127);
-          const float2 uv = s_uv[m8];
-          const float u = uv.x * d, w = uv.y * d;  // (exact: d is a power of two in the normal range)
-          tq[0] = 0.0f;
-          tq[1] = 0.5f * u;
-          tq[2] = u;
-          tq[3] = w;
-          tq[4] = 2.0f * u;
-          tq[5] = 2.0f * w;
-          tq[6] = 4.0f * u;
-          tq[7] = 4.0f * w;
-        }
-        if (MXQ_MBSD_SMEM_TQ && fast) {
-          double* tqd = s_tq + threadIdx.x * 17;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            tqd[k] = (double)tq[k];
-            tqd[8 + k] = -(double)tq[k];
+          for (int i = 0; i < 16; ++i) y[i] = __fmul_rn(v[i], f);
+          const bool fast = biased >= 4 && biased <= 250;
+          float tq[8];
+          if (fast) {
+            const float d = exp2i_f32((int)biased - 127);
+            const float2 uv = s_uv[m8];
+            const float u = uv.x * d, w = uv.y * d;  // (exact: d is a power of two in the normal range)
+            tq[0] = 0.0f;
+            tq[1] = 0.5f * u;
+            tq[2] = u;
+            tq[3] = w;
+            tq[4] = 2.0f * u;
+            tq[5] = 2.0f * w;
+            tq[6] = 4.0f * u;
+            tq[7] = 4.0f * w;
           }
+          if (MXQ_MBSD_SMEM_TQ && fast) {
+            tq_t* tqd = s_tq + threadIdx.x * 17;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              tqd[k] = (tq_t)tq[k];
+              tqd[8 + k] = -(tq_t)tq[k];
+            }
+#pragma unroll
+            for (int i = 0; i < 16; i += 2) {
+              const uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const double diff = __dsub_rn((double)tqd[(c2 >> (4 * h)) & 15u], (double)v[i + h]);
+                mb[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
+              }
+            }
+          } else {
 #pragma unroll
           for (int i = 0; i < 16; i += 2) {
-            const uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
+            uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const double diff = __dsub_rn(tqd[(c2 >> (4 * h)) & 15u], (double)v[i + h]);
-              mine[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
+              const uint32_t c = (c2 >> (4 * h)) & 15u;
+              float dq;
+              if (fast) {
+                dq = tq[c & 7];
+                dq = (c & 8u) ? -dq : dq;
+              } else {
+                dq = deq_mbs(c, biased, m8);
+              }
+              const double diff = __dsub_rn((double)dq, (double)v[i + h]);
+              mb[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
             }
           }
-        } else {
-#pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-          uint32_t c2 = e2m1x2(__fmul_rn(y[i], sf), __fmul_rn(y[i + 1], sf));
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t c = (c2 >> (4 * h)) & 15u;
-            float dq;
-            if (fast) {
-              dq = tq[c & 7];
-              dq = (c & 8u) ? -dq : dq;
-            } else {
-              dq = deq_mbs(c, biased, m8);
-            }
-            const double diff = __dsub_rn((double)dq, (double)v[i + h]);
-            mine[i + h] = active ? __dmul_rn(diff, diff) : 0.0;
           }
         }
-        }
-      }
-      __syncwarp();
-      double sse = 0.0;
-      if (g.G == 8) {
-        // full 128-element macros: numpy's eight strided accumulators, one per
-        // lane of the group (r_j = sq[j] + sq[j+8] + ... in ascending order),
-        // then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles -- the same
-        // operations in the same order as pw_leaf, 16 dependent adds per lane
-        // instead of 128 by one lane
-        // element sub + 8k sits in lane slot k/2, position sub + 8 (k % 2)
-        const double* cb = gbase + sub;
-        double r = cb[0];
+        return m8;
+    };
+    // A full 128-element macro's eight strided accumulators (numpy's leaf
+    // order): r_j = sq[j] + sq[j+8] + ... in ascending order, one per lane of
+    // the group (element sub + 8k sits in lane slot k/2, position sub + 8 (k % 2)).
+    auto lane_chain = [&](const double* gb) -> double {
+      const double* cb = gb + sub;
+      double r = cb[0];
 #pragma unroll
-        for (int k = 1; k < 16; ++k) r = __dadd_rn(r, cb[(k >> 1) * MBSD_STRIDE + 8 * (k & 1)]);
-        r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));  // r0+r1, r2+r3, ...
-        r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 2));  // (r0+r1)+(r2+r3), ...
-        r = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 4));  // the macro's sum at sub 0
-        if (sub == 0 && live_group) sse = width == 128 ? r : pw_sum_smem(gbase, 0, width);
-      } else if (sub == 0 && live_group) {
-        sse = pw_sum_smem(gbase, 0, width);
-      }
-      __syncwarp();
+      for (int k = 1; k < 16; ++k) r = __dadd_rn(r, cb[(k >> 1) * MBSD_STRIDE + 8 * (k & 1)]);
+      return r;
+    };
+    auto take = [&](int t, uint32_t m8, double sse) {
       if (sub == 0) {
         const bool better = (t == 0) || (sse < best_sse) || (sse == best_sse && m8 < best_m8);
         if (better) { best_sse = sse; best_m8 = m8; }
       }
+    };
+    // Trials in pairs (exact mode): both trials' errors are staged in two
+    // buffers and their accumulator chains and shuffle trees run interleaved --
+    // each is a dependent f64 chain, and the kernel was latency-bound on them.
+    // The argmin is taken in trial order, as before.
+    constexpr int PAIR = (!LUT && MXQ_MBSD_PAIR) ? 2 : 1;
+    for (int t0 = 0; t0 < n_trials; t0 += PAIR) {
+      const bool two = PAIR == 2 && t0 + 1 < n_trials;
+      const uint32_t m8a = elem_pass(t0, mine);
+      uint32_t m8b = 0;
+      if (two) m8b = elem_pass(t0 + 1, mine + MBSD_BUF);
+      __syncwarp();
+      double sa = 0.0, sb = 0.0;
+      if (g.G == 8) {
+        // ... then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles -- the same
+        // operations in the same order as pw_leaf
+        double ra = lane_chain(gbase), rb = two ? lane_chain(gbase + MBSD_BUF) : 0.0;
+        ra = __dadd_rn(ra, __shfl_down_sync(0xffffffffu, ra, 1));  // r0+r1, r2+r3, ...
+        rb = __dadd_rn(rb, __shfl_down_sync(0xffffffffu, rb, 1));
+        ra = __dadd_rn(ra, __shfl_down_sync(0xffffffffu, ra, 2));  // (r0+r1)+(r2+r3), ...
+        rb = __dadd_rn(rb, __shfl_down_sync(0xffffffffu, rb, 2));
+        ra = __dadd_rn(ra, __shfl_down_sync(0xffffffffu, ra, 4));  // the macro's sum at sub 0
+        rb = __dadd_rn(rb, __shfl_down_sync(0xffffffffu, rb, 4));
+        if (sub == 0 && live_group) {
+          sa = width == 128 ? ra : pw_sum_smem(gbase, 0, width);
+          if (two) sb = width == 128 ? rb : pw_sum_smem(gbase + MBSD_BUF, 0, width);
+        }
+      } else if (sub == 0 && live_group) {
+        sa = pw_sum_smem(gbase, 0, width);
+        if (two) sb = pw_sum_smem(gbase + MBSD_BUF, 0, width);
+      }
+      __syncwarp();
+      take(t0, m8a, sa);
+      if (two) take(t0 + 1, m8b, sb);
     }
     const uint32_t m8 = __shfl_sync(0xffffffffu, best_m8, lane & ~(g.G - 1));
     uint32_t packed[2];
